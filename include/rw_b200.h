@@ -1,0 +1,237 @@
+/* rw_b200.h — C-ABI of the B200-native RouterWise setup-search inner loop.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no C++ or
+ * torch types.  Every entry point replaces one function of the reference C++ solver
+ * API (/root/reference/proj/include/routeplan/...); the replaced interface is cited on
+ * each declaration.  INTEGRATION.md shows the C++ forwarding shim a maintainer adds so
+ * the reference's host code (runner.cpp:160-172 `run_search`) links against this.
+ *
+ * Conventions
+ *  - scores: row-major N x M doubles, `scores[j * M + i]` (workload.hpp:15).
+ *  - model order is the score-matrix column order (setup_search.cpp:160-161).
+ *  - latency profiles: CSR table; profile p has knots [knot_offsets[p], knot_offsets[p+1])
+ *    with strictly increasing load, first load 0 after ingestion (latency.cpp:375-393).
+ *    A setup names one profile per model (`profile_index[k * M + i]`), i.e. the
+ *    (model, tp, round(rho*1e4), metric) key lookup of latency.cpp:12,331 is resolved by
+ *    the host before the call.
+ *  - all calls are synchronous w.r.t. the host unless stated; results are bit-identical to
+ *    the reference CPU solver.
+ *  - errors: every function returns an rw_status; the message is available from
+ *    rw_last_error(ctx).  RW_ERR_VALIDATION / RW_ERR_CONFIG carry the same text the
+ *    reference's ValidationError / ConfigError would (errors.hpp:9-18).
+ *  - M <= RW_MAX_MODELS (device register tiles); larger M returns RW_ERR_UNSUPPORTED.
+ */
+#ifndef RW_B200_H
+#define RW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RW_ABI_VERSION 1
+#define RW_MAX_MODELS 32
+#define RW_MAX_TRACE 128
+
+typedef enum {
+  RW_OK = 0,
+  RW_ERR_VALIDATION = 1,  /* routeplan::ValidationError */
+  RW_ERR_CONFIG = 2,      /* routeplan::ConfigError */
+  RW_ERR_CUDA = 3,
+  RW_ERR_NCCL = 4,
+  RW_ERR_UNSUPPORTED = 5
+} rw_status;
+
+typedef struct rw_ctx rw_ctx; /* owns device buffers + a stream on one GPU */
+
+/* score_dual.hpp:46-52 SubgradientParams (init_alpha passed separately). */
+typedef struct {
+  double eta0;
+  int32_t max_iters;
+  double residual_tol;
+  int32_t polish_passes;
+} rw_subgradient_params;
+
+/* routing_opt.hpp:27-34 PgaParams (no on_iterate hook). */
+typedef struct {
+  double eta;
+  int32_t max_iters;
+  double w_tol;
+  rw_subgradient_params dual;
+} rw_pga_params;
+
+/* routing_opt.hpp:69-74 BetaSearchParams. */
+typedef struct {
+  double beta_min;
+  double beta_max; /* < 0 -> 10 / tau */
+  double epsilon;  /* < 0 -> (beta_max - beta_min) / 1024 */
+  rw_pga_params pga;
+} rw_beta_params;
+
+/* routing_opt.hpp:18-25 OptimizeContext minus the pointers (scores/profiles live in ctx). */
+typedef struct {
+  double lambda_rps;
+  double tau_ms;
+  double kappa;
+} rw_opt_context;
+
+/* score_dual.hpp:49-58 DualSolution (+ realised per-model counts after repair). */
+typedef struct {
+  double alpha_star[RW_MAX_MODELS];
+  double count_residual[RW_MAX_MODELS];
+  int32_t counts[RW_MAX_MODELS];
+  double score;
+  double dual_bound;
+  double duality_gap;
+  int32_t iterations;
+  int32_t converged;
+  int64_t eval_passes; /* eval_dual-equivalent passes executed (SURVEY §8d "evals") */
+} rw_dual_solution;
+
+/* routing_opt.hpp:36-44 RelaxedSolveResult. out_of_range is a bit mask over models. */
+typedef struct {
+  double w[RW_MAX_MODELS];
+  double objective;
+  double score;
+  double latency_ms;
+  int32_t iterations;
+  int32_t converged;
+  uint32_t out_of_range;
+  int32_t pad_;
+  int64_t eval_passes;
+} rw_relaxed_result;
+
+/* routing_opt.hpp:57-62 BetaStep. */
+typedef struct {
+  double beta;
+  double score;
+  double latency_ms;
+  int32_t feasible;
+  int32_t pad_;
+} rw_beta_step;
+
+/* routing_opt.hpp:67-73 BetaSearchResult (trace returned separately). */
+typedef struct {
+  int32_t feasible;
+  int32_t has_beta_star;
+  double beta_star;
+  double w_star[RW_MAX_MODELS];
+  rw_relaxed_result best;
+  int32_t n_trace;
+  int32_t pad_;
+  int64_t eval_passes;
+} rw_beta_result;
+
+/* One retained setup's outcome: the `Eval` of setup_search.cpp:177-184 plus the sweep
+ * record id (setup_search.hpp:45-51) and instrumentation.  Fixed size so records can be
+ * gathered across GPUs with one collective. */
+typedef struct {
+  int64_t setup_id;
+  int32_t feasible;
+  int32_t status; /* rw_status of this setup's solve */
+  double score;
+  double latency_ms;
+  double beta;
+  double w[RW_MAX_MODELS];
+  uint32_t out_of_range;
+  int32_t bisect_steps;
+  int64_t eval_passes;
+  int64_t polish_passes;
+  int64_t repair_calls;
+} rw_setup_record;
+
+/* ---- lifecycle ------------------------------------------------------------------- */
+int rw_abi_version(void);
+int rw_create(int device, rw_ctx** out);
+void rw_destroy(rw_ctx* ctx);
+/* Last error message of ctx (or of the calling thread when ctx is NULL). */
+const char* rw_last_error(const rw_ctx* ctx);
+/* Launch all work on this cudaStream_t (NULL = the ctx's own stream). */
+int rw_set_stream(rw_ctx* ctx, void* cuda_stream);
+/* Device time of the last solver kernel launch (CUDA events on the launch stream). */
+int rw_last_kernel_ms(const rw_ctx* ctx, double* ms);
+
+/* ---- inputs ------------------------------------------------------------------------ */
+/* Copy the N x M score matrix from host memory into the ctx's HBM buffer
+ * (replaces ScoreMatrix ownership, workload.hpp:12-23; values validated like
+ * ScoreMatrix::validate, workload.cpp:12-30). */
+int rw_load_scores(rw_ctx* ctx, int32_t n, int32_t m, const double* host_scores);
+/* Borrow an already-resident device matrix (caller keeps it alive). */
+int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* device_scores);
+/* Upload the latency profile table (replaces ProfileLibrary, latency.hpp:36-42;
+ * validated like LatencyProfile::validate, latency.cpp:296-308). */
+int rw_load_profiles(rw_ctx* ctx, int32_t n_profiles, const int64_t* knot_offsets,
+                     const double* knot_load, const double* knot_latency);
+
+/* ---- solver entry points (one setup / one price vector) ---------------------------- */
+/* score_dual.hpp:64-65 dual_objective(scores, targets, prices). */
+int rw_dual_objective(rw_ctx* ctx, const double* targets, const double* alpha, double* g);
+/* score_dual.hpp:60-61 assign_prompts(scores, prices); m_alpha must equal M. */
+int rw_assign_prompts(rw_ctx* ctx, int32_t m_alpha, const double* alpha, int32_t* model_of,
+                      int32_t* counts);
+/* score_dual.hpp:73-74 solve_dual(scores, targets, params); init_alpha may be NULL.
+ * assignment (N ints) may be NULL. */
+int rw_solve_dual(rw_ctx* ctx, const double* targets, const rw_subgradient_params* params,
+                  const double* init_alpha, rw_dual_solution* out, int32_t* assignment);
+/* routing_opt.hpp:15 project_simplex(v). Runs the device routine on one vector. */
+int rw_project_simplex(rw_ctx* ctx, int32_t m, const double* v, double* w);
+/* latency.hpp:52-77 system_latency_eval + system_latency_grad for one setup. */
+int rw_system_latency_eval(rw_ctx* ctx, const int32_t* profile_index, const double* w,
+                           double lambda_rps, double kappa, double* latency_ms,
+                           double* per_model_load, double* per_model_latency,
+                           int32_t* out_of_range, double* grad);
+/* routing_opt.hpp:50-51 optimize_fractions(setup, beta, ctx, params). */
+int rw_optimize_fractions(rw_ctx* ctx, const int32_t* profile_index, double beta,
+                          const rw_opt_context* opt, const rw_pga_params* params,
+                          rw_relaxed_result* out);
+/* routing_opt.hpp:79-80 optimize_beta(setup, ctx, params); trace may be NULL. */
+int rw_optimize_beta(rw_ctx* ctx, const int32_t* profile_index, const rw_opt_context* opt,
+                     const rw_beta_params* params, rw_beta_result* out, int32_t trace_cap,
+                     rw_beta_step* trace);
+
+/* ---- the sweep (setup_search.cpp:154-272, per-setup half) --------------------------- */
+/* Solve every retained setup k with k % shard_count == shard_rank (interleaved sharding,
+ * SURVEY §8e) on this GPU in one persistent kernel; writes one record per solved setup, in
+ * increasing k, to out_records (capacity >= ceil(n_setups / shard_count)).
+ * profile_index is n_setups x M; setup_ids are the enumeration ordinals. */
+int rw_sweep(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+             const int32_t* profile_index, const rw_opt_context* opt,
+             const rw_beta_params* params, int32_t shard_rank, int32_t shard_count,
+             rw_setup_record* out_records, int64_t* n_out);
+/* Same, asynchronous: records stay in device memory (ctx-owned) until rw_sweep_fetch. */
+int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                   const int32_t* profile_index, const rw_opt_context* opt,
+                   const rw_beta_params* params, int32_t shard_rank, int32_t shard_count);
+int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out_records, int64_t* n_out);
+
+/* Order-deterministic winner (setup_search.cpp:246-253): feasible, max score, then min
+ * latency, then smallest setup_id.  Records may come from any number of shards in any
+ * order.  Returns the record index or -1. */
+int64_t rw_reduce_records(int64_t n, const rw_setup_record* records);
+
+/* ---- host-side input producers ------------------------------------------------------ */
+/* workload.cpp:78-112 synth_scores: Beta(a_i, b_i) columns via mt19937_64 + libstdc++
+ * gamma_distribution, model-major draw order; identical matrix on this platform. */
+int rw_synth_scores(int32_t n, int32_t m, const double* shape_a, const double* shape_b,
+                    uint64_t seed, double* out);
+
+/* setup_search.cpp:99-152 enumerate_setups + retain.  Choices per model in CSR form,
+ * memory table entries (model, tp, fraction).  name_rank[i] is model i's rank in byte-wise
+ * name order (FFD breaks size ties by model name, setup_search.cpp:76-79); NULL = index order.
+ * Writes verdict per enumerated setup
+ * (0 RETAINED, 1 UNDER_UTILIZED, 2 OVER_BUDGET, 3 PLACEMENT_INFEASIBLE) and its (tp, rho)
+ * per model, up to cap setups; *n_enumerated gets the total. */
+int rw_enumerate_retain(int32_t m, const int32_t* name_rank, const int32_t* tp_offsets,
+                        const int32_t* tp_values, const int32_t* rho_offsets,
+                        const double* rho_values, int32_t n_mem, const int32_t* mem_model,
+                        const int32_t* mem_tp, const double* mem_fraction, int32_t gpu_count,
+                        double rho_floor,
+                        int64_t cap, int64_t* n_enumerated, int32_t* verdict, int32_t* tp_out,
+                        double* rho_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RW_B200_H */

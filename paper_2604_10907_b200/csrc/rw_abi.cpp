@@ -1,0 +1,665 @@
+// rw_abi.cpp — the C-ABI (include/rw_b200.h): context, input upload, validation with the
+// reference's error texts, job launch and result download.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rw_b200.h"
+#include "rw_job.h"
+
+struct rw_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  // scores
+  const double* d_scores = nullptr;
+  double* d_scores_owned = nullptr;
+  size_t scores_cap = 0;  // doubles
+  int32_t n = 0, m = 0;
+  // profiles
+  int64_t* d_koff = nullptr;
+  double* d_kx = nullptr;
+  double* d_ky = nullptr;
+  int32_t n_prof = 0;
+  std::vector<int64_t> h_koff;
+  // workspace
+  uint8_t* d_mo = nullptr;
+  uint64_t* d_keys = nullptr;
+  size_t ws_entries = 0;  // slots * n capacity
+  // generic io
+  void* d_io = nullptr;
+  size_t io_cap = 0;
+  unsigned long long* d_queue = nullptr;
+  int32_t* d_status = nullptr;
+  // sweep
+  int32_t* d_prof_idx = nullptr;
+  size_t prof_idx_cap = 0;
+  int64_t* d_setup_ids = nullptr;
+  size_t setup_ids_cap = 0;
+  rw_setup_record* d_records = nullptr;
+  size_t records_cap = 0;
+  int64_t pending_records = -1;
+  // timing
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  bool timed = false;
+  std::string err;
+};
+
+namespace {
+
+thread_local std::string g_tls_err;
+
+int set_err(rw_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  else g_tls_err = msg;
+  return code;
+}
+
+int cuda_err(rw_ctx* ctx, cudaError_t e, const char* where) {
+  return set_err(ctx, RW_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call)                                              \
+  do {                                                        \
+    cudaError_t e_ = (call);                                  \
+    if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call);   \
+  } while (0)
+
+// libstdc++'s std::to_string(double) (the reference builds its messages with it).
+std::string dstr(double x) { return std::to_string(x); }
+
+int ensure(rw_ctx* ctx, void** p, size_t* cap, size_t bytes) {
+  if (*cap >= bytes && *p) return RW_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  size_t b = std::max<size_t>(bytes, 256);
+  CK(cudaMalloc(p, b));
+  *cap = b;
+  return RW_OK;
+}
+
+int ensure_ws(rw_ctx* ctx, int slots) {
+  size_t need = (size_t)slots * (size_t)ctx->n;
+  if (ctx->ws_entries >= need && ctx->d_mo) return RW_OK;
+  if (ctx->d_mo) cudaFree(ctx->d_mo);
+  if (ctx->d_keys) cudaFree(ctx->d_keys);
+  ctx->d_mo = nullptr;
+  ctx->d_keys = nullptr;
+  ctx->ws_entries = 0;
+  CK(cudaMalloc(&ctx->d_mo, std::max<size_t>(need, 1)));
+  CK(cudaMalloc(&ctx->d_keys, std::max<size_t>(need, 1) * sizeof(uint64_t)));
+  ctx->ws_entries = need;
+  return RW_OK;
+}
+
+int need_inputs(rw_ctx* ctx, bool profiles) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (!ctx->d_scores || ctx->n <= 0 || ctx->m <= 0)
+    return set_err(ctx, RW_ERR_VALIDATION, "score matrix is empty");
+  if (ctx->m > RW_MAX_MODELS)
+    return set_err(ctx, RW_ERR_UNSUPPORTED,
+                   "rw_b200 supports at most " + std::to_string(RW_MAX_MODELS) + " models");
+  if (profiles && !ctx->d_koff)
+    return set_err(ctx, RW_ERR_VALIDATION, "optimizer context: missing scores or profiles");
+  return RW_OK;
+}
+
+// TargetCounts::validate (score_dual.cpp:195-205)
+int validate_targets(rw_ctx* ctx, const double* c) {
+  for (int i = 0; i < ctx->m; ++i)
+    if (!std::isfinite(c[i]) || c[i] < -1e-9)
+      return set_err(ctx, RW_ERR_VALIDATION,
+                     "target counts: entry " + std::to_string(i) + " is negative");
+  double t = 0.0;
+  for (int i = 0; i < ctx->m; ++i) t += c[i];
+  if (std::abs(t - ctx->n) > 1e-6 * std::max(1.0, static_cast<double>(ctx->n)))
+    return set_err(ctx, RW_ERR_VALIDATION,
+                   "target counts sum to " + dstr(t) + ", expected " + std::to_string(ctx->n));
+  return RW_OK;
+}
+
+int validate_profile_index(rw_ctx* ctx, const int32_t* pidx, size_t count) {
+  for (size_t k = 0; k < count; ++k)
+    if (pidx[k] < 0 || pidx[k] >= ctx->n_prof)
+      return set_err(ctx, RW_ERR_CONFIG,
+                     "no latency profile for index " + std::to_string(pidx[k]));
+  return RW_OK;
+}
+
+rw::Job base_job(rw_ctx* ctx, int kind) {
+  rw::Job j;
+  std::memset(&j, 0, sizeof(j));
+  j.kind = kind;
+  j.n = ctx->n;
+  j.m = ctx->m;
+  j.scores = ctx->d_scores;
+  j.koff = ctx->d_koff;
+  j.kx = ctx->d_kx;
+  j.ky = ctx->d_ky;
+  j.shard_count = 1;
+  j.ws_model_of = ctx->d_mo;
+  j.ws_keys = ctx->d_keys;
+  j.queue = ctx->d_queue;
+  j.status_out = ctx->d_status;
+  return j;
+}
+
+// Launch + time + wait; maps device status to an error.
+int run(rw_ctx* ctx, rw::Job& j, int grid) {
+  j.ws_model_of = ctx->d_mo;
+  j.ws_keys = ctx->d_keys;
+  CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int32_t), ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(unsigned long long), ctx->stream));
+  CK(cudaEventRecord(ctx->ev0, ctx->stream));
+  int e = rw::launch_job(j, grid, ctx->stream);
+  if (e != 0) return cuda_err(ctx, (cudaError_t)e, "solver_kernel launch");
+  CK(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->timed = true;
+  return RW_OK;
+}
+
+int finish(rw_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  int32_t st = 0;
+  CK(cudaMemcpy(&st, ctx->d_status, sizeof(st), cudaMemcpyDeviceToHost));
+  if (st == RW_ERR_VALIDATION)
+    return set_err(ctx, RW_ERR_VALIDATION,
+                   "solver: invalid intermediate state (non-finite or inconsistent targets)");
+  if (st) return set_err(ctx, st, "solver: device status " + std::to_string(st));
+  return RW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rw_abi_version(void) { return RW_ABI_VERSION; }
+
+int rw_create(int device, rw_ctx** out) {
+  if (!out) return set_err(nullptr, RW_ERR_VALIDATION, "rw_create: null out");
+  *out = nullptr;
+  rw_ctx* ctx = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_err(nullptr, e, "cudaSetDevice");
+  ctx = new rw_ctx();
+  ctx->device = device;
+#define CKC(call)                          \
+  do {                                     \
+    cudaError_t e2 = (call);               \
+    if (e2 != cudaSuccess) {               \
+      int rc = cuda_err(nullptr, e2, #call); \
+      rw_destroy(ctx);                     \
+      return rc;                           \
+    }                                      \
+  } while (0)
+  CKC(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  CKC(cudaEventCreate(&ctx->ev0));
+  CKC(cudaEventCreate(&ctx->ev1));
+  CKC(cudaMalloc(&ctx->d_queue, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->d_status, sizeof(int32_t)));
+#undef CKC
+  *out = ctx;
+  return RW_OK;
+}
+
+void rw_destroy(rw_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_scores_owned);
+  cudaFree(ctx->d_koff);
+  cudaFree(ctx->d_kx);
+  cudaFree(ctx->d_ky);
+  cudaFree(ctx->d_mo);
+  cudaFree(ctx->d_keys);
+  cudaFree(ctx->d_io);
+  cudaFree(ctx->d_queue);
+  cudaFree(ctx->d_status);
+  cudaFree(ctx->d_prof_idx);
+  cudaFree(ctx->d_setup_ids);
+  cudaFree(ctx->d_records);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* rw_last_error(const rw_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_tls_err.c_str();
+}
+
+int rw_set_stream(rw_ctx* ctx, void* stream) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return RW_OK;
+}
+
+int rw_last_kernel_ms(const rw_ctx* ctx, double* ms) {
+  if (!ctx || !ms || !ctx->timed) return RW_ERR_VALIDATION;
+  float f = 0.f;
+  if (cudaEventElapsedTime(&f, ctx->ev0, ctx->ev1) != cudaSuccess) return RW_ERR_CUDA;
+  *ms = f;
+  return RW_OK;
+}
+
+int rw_load_scores(rw_ctx* ctx, int32_t n, int32_t m, const double* host) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (n <= 0) return set_err(ctx, RW_ERR_VALIDATION, "score matrix: no prompts");
+  if (m <= 0) return set_err(ctx, RW_ERR_VALIDATION, "score matrix: no models");
+  if (m > RW_MAX_MODELS)
+    return set_err(ctx, RW_ERR_UNSUPPORTED,
+                   "rw_b200 supports at most " + std::to_string(RW_MAX_MODELS) + " models");
+  const size_t cnt = (size_t)n * (size_t)m;
+  for (size_t k = 0; k < cnt; ++k) {  // ScoreMatrix::validate (workload.cpp:23-29)
+    double v = host[k];
+    if (!std::isfinite(v) || v < 0.0 || v > 1.0) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%.17g", v);
+      return set_err(ctx, RW_ERR_VALIDATION,
+                     "score matrix: entry for prompt 'p" + std::to_string(k / m + 1) +
+                         "', model " + std::to_string(k % m) + " is " + buf +
+                         ", outside [0, 1]");
+    }
+  }
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->scores_cap < cnt || !ctx->d_scores_owned) {
+    cudaFree(ctx->d_scores_owned);
+    ctx->d_scores_owned = nullptr;
+    ctx->scores_cap = 0;
+    CK(cudaMalloc(&ctx->d_scores_owned, cnt * sizeof(double)));
+    ctx->scores_cap = cnt;
+  }
+  CK(cudaMemcpyAsync(ctx->d_scores_owned, host, cnt * sizeof(double), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  ctx->d_scores = ctx->d_scores_owned;
+  ctx->n = n;
+  ctx->m = m;
+  return RW_OK;
+}
+
+int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* dev) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (n <= 0 || m <= 0 || !dev) return set_err(ctx, RW_ERR_VALIDATION, "score matrix is empty");
+  if (m > RW_MAX_MODELS)
+    return set_err(ctx, RW_ERR_UNSUPPORTED,
+                   "rw_b200 supports at most " + std::to_string(RW_MAX_MODELS) + " models");
+  if ((reinterpret_cast<uintptr_t>(dev) & 15u) != 0)
+    return set_err(ctx, RW_ERR_VALIDATION, "device score matrix must be 16-byte aligned");
+  ctx->d_scores = dev;
+  ctx->n = n;
+  ctx->m = m;
+  return RW_OK;
+}
+
+int rw_load_profiles(rw_ctx* ctx, int32_t np, const int64_t* koff, const double* kx,
+                     const double* ky) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (np <= 0) return set_err(ctx, RW_ERR_VALIDATION, "profile table: no profiles");
+  if (koff[0] != 0) return set_err(ctx, RW_ERR_VALIDATION, "profile table: offsets must start at 0");
+  for (int p = 0; p < np; ++p) {  // LatencyProfile::validate (latency.cpp:296-308)
+    int64_t a = koff[p], b = koff[p + 1];
+    std::string who = "profile " + std::to_string(p);
+    if (b - a < 2) return set_err(ctx, RW_ERR_VALIDATION, who + ": needs at least two knots");
+    for (int64_t k = a; k < b; ++k) {
+      if (kx[k] < 0.0 || ky[k] < 0.0)
+        return set_err(ctx, RW_ERR_VALIDATION, who + ": negative load or latency");
+      if (k > a && !(kx[k] > kx[k - 1]))
+        return set_err(ctx, RW_ERR_VALIDATION, who + ": loads must be strictly increasing");
+    }
+  }
+  CK(cudaSetDevice(ctx->device));
+  const int64_t nk = koff[np];
+  cudaFree(ctx->d_koff);
+  cudaFree(ctx->d_kx);
+  cudaFree(ctx->d_ky);
+  ctx->d_koff = nullptr;
+  ctx->d_kx = ctx->d_ky = nullptr;
+  CK(cudaMalloc(&ctx->d_koff, sizeof(int64_t) * (np + 1)));
+  CK(cudaMalloc(&ctx->d_kx, sizeof(double) * nk));
+  CK(cudaMalloc(&ctx->d_ky, sizeof(double) * nk));
+  CK(cudaMemcpy(ctx->d_koff, koff, sizeof(int64_t) * (np + 1), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_kx, kx, sizeof(double) * nk, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_ky, ky, sizeof(double) * nk, cudaMemcpyHostToDevice));
+  ctx->n_prof = np;
+  ctx->h_koff.assign(koff, koff + np + 1);
+  return RW_OK;
+}
+
+// ---- single pass -----------------------------------------------------------------------
+static int eval_job(rw_ctx* ctx, const double* targets, const double* alpha, double* g,
+                    int32_t* model_of, int32_t* counts) {
+  int rc;
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  const size_t n = ctx->n, m = ctx->m;
+  size_t bytes = sizeof(double) * 4 + sizeof(int32_t) * (m + n) + 64;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, bytes))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_EVAL);
+  for (size_t i = 0; i < m; ++i) {
+    j.c[i] = targets[i];
+    j.vec[i] = alpha[i];
+  }
+  char* io = static_cast<char*>(ctx->d_io);
+  j.dvec_out = reinterpret_cast<double*>(io);
+  j.ivec_out = reinterpret_cast<int32_t*>(io + 32);
+  j.assign_out = reinterpret_cast<int32_t*>(io + 32 + sizeof(int32_t) * m);
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  if (g) CK(cudaMemcpy(g, j.dvec_out, sizeof(double), cudaMemcpyDeviceToHost));
+  if (counts) CK(cudaMemcpy(counts, j.ivec_out, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+  if (model_of)
+    CK(cudaMemcpy(model_of, j.assign_out, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  return RW_OK;
+}
+
+int rw_dual_objective(rw_ctx* ctx, const double* targets, const double* alpha, double* g) {
+  int rc;
+  if ((rc = need_inputs(ctx, false))) return rc;
+  if ((rc = validate_targets(ctx, targets))) return rc;
+  return eval_job(ctx, targets, alpha, g, nullptr, nullptr);
+}
+
+int rw_assign_prompts(rw_ctx* ctx, int32_t m_alpha, const double* alpha, int32_t* model_of,
+                      int32_t* counts) {
+  int rc;
+  if ((rc = need_inputs(ctx, false))) return rc;
+  if (m_alpha != ctx->m)  // score_dual.cpp:214-216
+    return set_err(ctx, RW_ERR_VALIDATION,
+                   "prices have " + std::to_string(m_alpha) + " entries for " +
+                       std::to_string(ctx->m) + " models");
+  std::vector<double> zeros(ctx->m, 0.0);
+  return eval_job(ctx, zeros.data(), alpha, nullptr, model_of, counts);
+}
+
+int rw_solve_dual(rw_ctx* ctx, const double* targets, const rw_subgradient_params* params,
+                  const double* init_alpha, rw_dual_solution* out, int32_t* assignment) {
+  int rc;
+  if ((rc = need_inputs(ctx, false))) return rc;
+  if ((rc = validate_targets(ctx, targets))) return rc;
+  if (!params || !out) return set_err(ctx, RW_ERR_VALIDATION, "rw_solve_dual: null argument");
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  const size_t n = ctx->n, m = ctx->m;
+  size_t bytes = sizeof(rw_dual_solution) + 64 + sizeof(int32_t) * n;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, bytes))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_SOLVE);
+  for (size_t i = 0; i < m; ++i) {
+    j.c[i] = targets[i];
+    j.vec[i] = init_alpha ? init_alpha[i] : 0.0;
+  }
+  j.has_vec = init_alpha ? 1 : 0;
+  j.bp.pga.dual = *params;
+  char* io = static_cast<char*>(ctx->d_io);
+  j.dual_out = reinterpret_cast<rw_dual_solution*>(io);
+  j.assign_out = reinterpret_cast<int32_t*>(io + ((sizeof(rw_dual_solution) + 63) / 64) * 64);
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  CK(cudaMemcpy(out, j.dual_out, sizeof(rw_dual_solution), cudaMemcpyDeviceToHost));
+  if (assignment)
+    CK(cudaMemcpy(assignment, j.assign_out, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  return RW_OK;
+}
+
+int rw_project_simplex(rw_ctx* ctx, int32_t m, const double* v, double* w) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (m <= 0) return set_err(ctx, RW_ERR_VALIDATION, "project_simplex: empty input");
+  if (m > RW_MAX_MODELS) return set_err(ctx, RW_ERR_UNSUPPORTED, "project_simplex: too many entries");
+  for (int i = 0; i < m; ++i)
+    if (!std::isfinite(v[i]))
+      return set_err(ctx, RW_ERR_VALIDATION, "project_simplex: non-finite input");
+  int rc;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, sizeof(double) * RW_MAX_MODELS))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_SIMPLEX);
+  j.n = 1;
+  j.m = m;
+  for (int i = 0; i < m; ++i) j.vec[i] = v[i];
+  j.dvec_out = static_cast<double*>(ctx->d_io);
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  CK(cudaMemcpy(w, j.dvec_out, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  return RW_OK;
+}
+
+static int upload_pidx(rw_ctx* ctx, const int32_t* pidx, size_t count) {
+  int rc;
+  void* p = ctx->d_prof_idx;
+  size_t cap = ctx->prof_idx_cap;
+  if ((rc = ensure(ctx, &p, &cap, sizeof(int32_t) * count))) return rc;
+  ctx->d_prof_idx = static_cast<int32_t*>(p);
+  ctx->prof_idx_cap = cap;
+  CK(cudaMemcpyAsync(ctx->d_prof_idx, pidx, sizeof(int32_t) * count, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return RW_OK;
+}
+
+// check_setup_and_w (latency.cpp:285-292) with RoutingFractions::validate(1e-4) (types.cpp:513)
+static int validate_w(rw_ctx* ctx, int m, const double* w) {
+  double tol = 1e-4, sum = 0.0;
+  for (int i = 0; i < m; ++i) {
+    if (!std::isfinite(w[i])) return set_err(ctx, RW_ERR_VALIDATION, "routing fractions: non-finite entry");
+    if (w[i] < -tol) return set_err(ctx, RW_ERR_VALIDATION, "routing fractions: negative entry");
+    sum += w[i];
+  }
+  if (std::abs(sum - 1.0) > tol)
+    return set_err(ctx, RW_ERR_VALIDATION,
+                   "routing fractions: entries sum to " + dstr(sum) + ", expected 1");
+  for (int i = 0; i < m; ++i)
+    if (w[i] < 0.0) return set_err(ctx, RW_ERR_VALIDATION, "latency_at: negative load");
+  return RW_OK;
+}
+
+int rw_system_latency_eval(rw_ctx* ctx, const int32_t* pidx, const double* w, double lambda,
+                           double kappa, double* latency, double* loads, double* lats,
+                           int32_t* oor, double* grad) {
+  int rc;
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (!ctx->d_koff) return set_err(ctx, RW_ERR_VALIDATION, "optimizer context: missing scores or profiles");
+  const int m = ctx->m > 0 ? ctx->m : 0;
+  if (m <= 0) return set_err(ctx, RW_ERR_VALIDATION, "score matrix is empty");
+  if ((rc = validate_profile_index(ctx, pidx, m))) return rc;
+  if ((rc = validate_w(ctx, m, w))) return rc;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, sizeof(double) * (1 + 3 * m) + 4 * m + 64)))
+    return rc;
+  if ((rc = upload_pidx(ctx, pidx, m))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_LATENCY);
+  j.prof_idx = ctx->d_prof_idx;
+  for (int i = 0; i < m; ++i) j.vec[i] = w[i];
+  j.opt.lambda_rps = lambda;
+  j.opt.kappa = kappa;
+  char* io = static_cast<char*>(ctx->d_io);
+  j.dvec_out = reinterpret_cast<double*>(io);
+  j.ivec_out = reinterpret_cast<int32_t*>(io + sizeof(double) * (1 + 3 * m));
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  std::vector<double> d(1 + 3 * m);
+  std::vector<int32_t> o(m);
+  CK(cudaMemcpy(d.data(), j.dvec_out, sizeof(double) * d.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(o.data(), j.ivec_out, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+  if (latency) *latency = d[0];
+  for (int i = 0; i < m; ++i) {
+    if (loads) loads[i] = d[1 + i];
+    if (lats) lats[i] = d[1 + m + i];
+    if (grad) grad[i] = d[1 + 2 * m + i];
+    if (oor) oor[i] = o[i];
+  }
+  return RW_OK;
+}
+
+// check_context (routing_opt.cpp:11-26)
+static int check_context(rw_ctx* ctx, const int32_t* pidx, const rw_opt_context* opt) {
+  int rc;
+  if ((rc = need_inputs(ctx, true))) return rc;
+  if (!opt) return set_err(ctx, RW_ERR_VALIDATION, "optimizer context: missing");
+  if (!(opt->lambda_rps > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "arrival rate must be positive");
+  if (!(opt->kappa > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "kappa must be positive");
+  return validate_profile_index(ctx, pidx, ctx->m);
+}
+
+int rw_optimize_fractions(rw_ctx* ctx, const int32_t* pidx, double beta,
+                          const rw_opt_context* opt, const rw_pga_params* params,
+                          rw_relaxed_result* out) {
+  int rc;
+  if ((rc = check_context(ctx, pidx, opt))) return rc;
+  if (!(beta >= 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "beta must be >= 0");
+  if (!params || !out) return set_err(ctx, RW_ERR_VALIDATION, "rw_optimize_fractions: null argument");
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, sizeof(rw_relaxed_result)))) return rc;
+  if ((rc = upload_pidx(ctx, pidx, ctx->m))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_OPTFRAC);
+  j.prof_idx = ctx->d_prof_idx;
+  j.opt = *opt;
+  j.beta = beta;
+  j.bp.pga = *params;
+  j.relaxed_out = static_cast<rw_relaxed_result*>(ctx->d_io);
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  CK(cudaMemcpy(out, j.relaxed_out, sizeof(rw_relaxed_result), cudaMemcpyDeviceToHost));
+  return RW_OK;
+}
+
+static int check_beta_params(rw_ctx* ctx, const rw_opt_context* opt, const rw_beta_params* p) {
+  double lo = p->beta_min, hi = p->beta_max;
+  if (hi < 0.0) {  // routing_opt.cpp:143-151
+    if (!(opt->tau_ms > 0.0))
+      return set_err(ctx, RW_ERR_VALIDATION,
+                     "latency target must be positive to derive default beta bounds");
+    hi = 10.0 / opt->tau_ms;
+  }
+  double eps = p->epsilon;
+  if (eps < 0.0) eps = (hi - lo) / 1024.0;
+  if (!(lo >= 0.0) || !(lo < hi))
+    return set_err(ctx, RW_ERR_VALIDATION, "beta bounds must satisfy 0 <= min < max");
+  if (!(eps > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "beta search epsilon must be positive");
+  return RW_OK;
+}
+
+int rw_optimize_beta(rw_ctx* ctx, const int32_t* pidx, const rw_opt_context* opt,
+                     const rw_beta_params* params, rw_beta_result* out, int32_t trace_cap,
+                     rw_beta_step* trace) {
+  int rc;
+  if ((rc = check_context(ctx, pidx, opt))) return rc;
+  if (!params || !out) return set_err(ctx, RW_ERR_VALIDATION, "rw_optimize_beta: null argument");
+  if ((rc = check_beta_params(ctx, opt, params))) return rc;
+  if (!trace) trace_cap = 0;
+  trace_cap = std::max(0, trace_cap);
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  size_t bytes = sizeof(rw_beta_result) + 64 + sizeof(rw_beta_step) * (size_t)trace_cap;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, bytes))) return rc;
+  if ((rc = upload_pidx(ctx, pidx, ctx->m))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_OPTBETA);
+  j.prof_idx = ctx->d_prof_idx;
+  j.opt = *opt;
+  j.bp = *params;
+  char* io = static_cast<char*>(ctx->d_io);
+  j.beta_out = reinterpret_cast<rw_beta_result*>(io);
+  j.trace_out = trace_cap ? reinterpret_cast<rw_beta_step*>(
+                                io + ((sizeof(rw_beta_result) + 63) / 64) * 64)
+                          : nullptr;
+  j.trace_cap = trace_cap;
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  CK(cudaMemcpy(out, j.beta_out, sizeof(rw_beta_result), cudaMemcpyDeviceToHost));
+  if (trace_cap) {
+    int32_t k = std::min(trace_cap, out->n_trace);
+    if (k > 0)
+      CK(cudaMemcpy(trace, j.trace_out, sizeof(rw_beta_step) * k, cudaMemcpyDeviceToHost));
+  }
+  return RW_OK;
+}
+
+int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                   const int32_t* pidx, const rw_opt_context* opt, const rw_beta_params* params,
+                   int32_t shard_rank, int32_t shard_count) {
+  int rc;
+  if ((rc = need_inputs(ctx, true))) return rc;
+  if (!opt || !params) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: null argument");
+  if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: bad shard");
+  if (n_setups < 0) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: negative setup count");
+  if (!(opt->lambda_rps > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "arrival rate must be positive");
+  if (!(opt->kappa > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "kappa must be positive");
+  if (n_setups > 0) {
+    if ((rc = check_beta_params(ctx, opt, params))) return rc;
+    if ((rc = validate_profile_index(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
+  }
+  const int64_t items =
+      n_setups > shard_rank ? (n_setups - shard_rank + shard_count - 1) / shard_count : 0;
+  ctx->pending_records = items;
+  if (items == 0) return RW_OK;
+  CK(cudaSetDevice(ctx->device));
+  if ((rc = upload_pidx(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
+  {
+    void* p = ctx->d_setup_ids;
+    size_t cap = ctx->setup_ids_cap;
+    if ((rc = ensure(ctx, &p, &cap, sizeof(int64_t) * n_setups))) return rc;
+    ctx->d_setup_ids = static_cast<int64_t*>(p);
+    ctx->setup_ids_cap = cap;
+    std::vector<int64_t> ids;
+    if (!setup_ids) {
+      ids.resize(n_setups);
+      for (int64_t k = 0; k < n_setups; ++k) ids[k] = k;
+      setup_ids = ids.data();
+    }
+    CK(cudaMemcpyAsync(ctx->d_setup_ids, setup_ids, sizeof(int64_t) * n_setups,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // `ids` is stack-owned
+  }
+  {
+    void* p = ctx->d_records;
+    size_t cap = ctx->records_cap;
+    if ((rc = ensure(ctx, &p, &cap, sizeof(rw_setup_record) * items))) return rc;
+    ctx->d_records = static_cast<rw_setup_record*>(p);
+    ctx->records_cap = cap;
+  }
+  int grid = (int)std::min<int64_t>(items, rw::sweep_max_resident(ctx->m, ctx->device));
+  if ((rc = ensure_ws(ctx, grid))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_SWEEP);
+  j.prof_idx = ctx->d_prof_idx;
+  j.setup_ids = ctx->d_setup_ids;
+  j.n_items = n_setups;
+  j.shard_rank = shard_rank;
+  j.shard_count = shard_count;
+  j.opt = *opt;
+  j.bp = *params;
+  j.records = ctx->d_records;
+  return run(ctx, j, grid);
+}
+
+int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out, int64_t* n_out) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (ctx->pending_records < 0) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep_fetch: no sweep");
+  int64_t items = ctx->pending_records;
+  ctx->pending_records = -1;
+  if (n_out) *n_out = items;
+  if (items == 0) return RW_OK;
+  int rc = finish(ctx);
+  if (rc) {
+    // per-record status names the first failing setup
+    std::vector<rw_setup_record> recs(items);
+    cudaMemcpy(recs.data(), ctx->d_records, sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost);
+    for (const auto& r : recs)
+      if (r.status)
+        return set_err(ctx, r.status, "setup " + std::to_string(r.setup_id) + ": " + ctx->err);
+    return rc;
+  }
+  if (out)
+    CK(cudaMemcpy(out, ctx->d_records, sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost));
+  return RW_OK;
+}
+
+int rw_sweep(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const int32_t* pidx,
+             const rw_opt_context* opt, const rw_beta_params* params, int32_t shard_rank,
+             int32_t shard_count, rw_setup_record* out, int64_t* n_out) {
+  int rc = rw_sweep_async(ctx, n_setups, setup_ids, pidx, opt, params, shard_rank, shard_count);
+  if (rc) return rc;
+  return rw_sweep_fetch(ctx, out, n_out);
+}
+
+}  // extern "C"

@@ -1,0 +1,2 @@
+#include "rw_inst.cuh"
+RW_INSTANTIATE(4, 8, 512)
