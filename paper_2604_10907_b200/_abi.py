@@ -102,6 +102,9 @@ def lib():
         L.rw_last_error.argtypes = [C.c_void_p]
         L.rw_set_stream.argtypes = [C.c_void_p, C.c_void_p]
         L.rw_last_kernel_ms.argtypes = [C.c_void_p, _dp]
+        L.rw_set_profiling.argtypes = [C.c_void_p, C.c_int]
+        L.rw_get_profile.argtypes = [C.c_void_p, _lp]
+        L.rw_bench_passes.argtypes = [C.c_void_p, _dp, _dp, C.c_int32, _dp]
         L.rw_load_scores.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _dp]
         L.rw_bind_scores_device.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.rw_load_profiles.argtypes = [C.c_void_p, C.c_int32, _lp, _dp, _dp]

@@ -47,6 +47,7 @@ struct rw_ctx {
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
+  long long* d_prof = nullptr;  // optional cycle counters (rw_set_profiling)
   std::string err;
 };
 
@@ -147,6 +148,7 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
   j.ws_keys = ctx->d_keys;
   j.queue = ctx->d_queue;
   j.status_out = ctx->d_status;
+  j.prof_out = ctx->d_prof;
   return j;
 }
 
@@ -225,6 +227,7 @@ void rw_destroy(rw_ctx* ctx) {
   cudaFree(ctx->d_prof_idx);
   cudaFree(ctx->d_setup_ids);
   cudaFree(ctx->d_records);
+  cudaFree(ctx->d_prof);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -246,6 +249,26 @@ int rw_last_kernel_ms(const rw_ctx* ctx, double* ms) {
   float f = 0.f;
   if (cudaEventElapsedTime(&f, ctx->ev0, ctx->ev1) != cudaSuccess) return RW_ERR_CUDA;
   *ms = f;
+  return RW_OK;
+}
+
+int rw_set_profiling(rw_ctx* ctx, int enable) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  CK(cudaSetDevice(ctx->device));
+  if (enable && !ctx->d_prof) CK(cudaMalloc(&ctx->d_prof, 8 * sizeof(long long)));
+  if (!enable && ctx->d_prof) {
+    cudaFree(ctx->d_prof);
+    ctx->d_prof = nullptr;
+  }
+  if (ctx->d_prof) CK(cudaMemset(ctx->d_prof, 0, 8 * sizeof(long long)));
+  return RW_OK;
+}
+
+int rw_get_profile(rw_ctx* ctx, int64_t* out8) {
+  if (!ctx || !ctx->d_prof) return set_err(ctx, RW_ERR_VALIDATION, "profiling not enabled");
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaMemcpy(out8, ctx->d_prof, 8 * sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->d_prof, 0, 8 * sizeof(long long)));
   return RW_OK;
 }
 
@@ -363,6 +386,27 @@ int rw_dual_objective(rw_ctx* ctx, const double* targets, const double* alpha, d
   if ((rc = need_inputs(ctx, false))) return rc;
   if ((rc = validate_targets(ctx, targets))) return rc;
   return eval_job(ctx, targets, alpha, g, nullptr, nullptr);
+}
+
+int rw_bench_passes(rw_ctx* ctx, const double* targets, const double* alpha, int32_t passes,
+                    double* g) {
+  int rc;
+  if ((rc = need_inputs(ctx, false))) return rc;
+  if ((rc = ensure_ws(ctx, 1))) return rc;
+  if ((rc = ensure(ctx, &ctx->d_io, &ctx->io_cap, 256 + sizeof(int32_t) * ctx->m))) return rc;
+  rw::Job j = base_job(ctx, rw::JOB_BENCH_PASS);
+  for (int i = 0; i < ctx->m; ++i) {
+    j.c[i] = targets[i];
+    j.vec[i] = alpha[i];
+  }
+  j.trace_cap = passes;
+  char* io = static_cast<char*>(ctx->d_io);
+  j.dvec_out = reinterpret_cast<double*>(io);
+  j.ivec_out = reinterpret_cast<int32_t*>(io + 64);
+  if ((rc = run(ctx, j, 1))) return rc;
+  if ((rc = finish(ctx))) return rc;
+  CK(cudaMemcpy(g, j.dvec_out, sizeof(double), cudaMemcpyDeviceToHost));
+  return RW_OK;
 }
 
 int rw_assign_prompts(rw_ctx* ctx, int32_t m_alpha, const double* alpha, int32_t* model_of,

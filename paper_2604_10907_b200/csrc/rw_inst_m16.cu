@@ -1,2 +1,2 @@
 #include "rw_inst.cuh"
-RW_INSTANTIATE(16, 8, 512)
+RW_INSTANTIATE(16, 24, 256)

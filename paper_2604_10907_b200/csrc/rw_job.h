@@ -15,6 +15,7 @@ enum JobKind : int32_t {
   JOB_SWEEP = 4,    // select_setup per-setup evaluate, persistent over a work queue
   JOB_SIMPLEX = 5,  // project_simplex on one vector
   JOB_LATENCY = 6,  // system_latency_eval + grad for one setup
+  JOB_BENCH_PASS = 7,  // diagnostics: trace_cap eval passes at fixed prices
 };
 
 struct Job {
@@ -52,6 +53,7 @@ struct Job {
   uint8_t* ws_model_of;
   uint64_t* ws_keys;
   unsigned long long* queue;
+  long long* prof_out;  // optional cycle counters [8] (debug)
 };
 
 // Host launcher (rw_kernels.cu). Returns a cudaError_t value.

@@ -72,14 +72,13 @@ template <int MM, int L, int T>
 struct Smem {
   static constexpr int R = L * T;       // rows per tile
   static constexpr int W = T / 32;      // warps
-  static constexpr int BPAD = R + R / 16;
-  double b[BPAD];                       // tile's b_j (padded: 1 slot per 16 against conflicts)
-  long long q0[T], q1[T];               // per-thread chunk quanta
-  long long wq0[W], wq1[W];             // per-warp composed quanta
+  static constexpr int BPAD = T * (L | 1);
+  double b[BPAD];                       // tile's b_j, chunk t at [t*(L|1), +L) (odd stride)
+  long long q0[T], q1[T];               // pieces: SAFE -> (Q0, Q1); RAW -> (start, count)
   double scan_x[W], scan_y[W];
   unsigned hist[256];
-  unsigned char safe[T];
-  unsigned char wuni[W];
+  unsigned char pkind[T];             // piece kind per slot (SAFE / RAW)
+  int wcnt[W];                         // pieces per warp
   // reduction scratch
   double red_d[W];
   int red_j[W];
@@ -98,6 +97,8 @@ struct Smem {
   // radix select
   unsigned long long sel_prefix;
   int sel_k;
+  int cand_n, above_n;
+  double pol_delta;
   // optimize_fractions state
   double w[MM], best_w[MM], warm[MM], grad[MM], step[MM], nextw[MM], tmp[MM];
   double best_obj;
@@ -115,6 +116,7 @@ struct Smem {
   double tr_best_lat, tr_best_score;
   // counters
   long long eval_passes, polish_passes, repair_calls;
+  long long prof[8];  // cycle counters (debug: Job.prof_out)
   long long cur_item;
 };
 
@@ -213,6 +215,16 @@ __device__ inline bool project_simplex(int m, const double* v, double* w, double
 // The solver: all threads of the CTA execute every member function (uniform control
 // flow); scalar state lives in shared memory and is updated by thread 0 between barriers.
 enum PassMode { PASS_EVAL = 0, PASS_FIXED = 1 };
+enum PieceKind { PIECE_NONE = 0, PIECE_SAFE = 1, PIECE_RAW = 2 };
+
+// Shared memory is always reached through the extern __shared__ symbol so every access
+// compiles to LDS/STS (a reference member would decay to generic LD/ST).
+template <class SMT>
+__device__ __forceinline__ SMT& smem() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return *reinterpret_cast<SMT*>(smem_raw);
+}
+#define SMX (smem<SM>())
 
 template <int MM, int L, int T>
 struct Solver {
@@ -221,7 +233,6 @@ struct Solver {
   static constexpr int W = SM::W;
   static constexpr int NPK = (MM + 3) / 4;  // packed 16-bit count words
 
-  SM& sm;
   const Job& jb;
   const int n, m;
   const int tid, lane, wid;
@@ -229,75 +240,136 @@ struct Solver {
   unsigned long long* keys;  // this CTA's radix-select workspace [n]
   const int32_t* pidx;       // current setup's profile indices [m]
 
-  __device__ Solver(SM& s, const Job& j, uint8_t* mo_, unsigned long long* keys_)
-      : sm(s), jb(j), n(j.n), m(j.m), tid(threadIdx.x), lane(threadIdx.x & 31),
+  __device__ Solver(const Job& j, uint8_t* mo_, unsigned long long* keys_)
+      : jb(j), n(j.n), m(j.m), tid(threadIdx.x), lane(threadIdx.x & 31),
         wid(threadIdx.x >> 5), mo(mo_), keys(keys_), pidx(nullptr) {}
 
-  __device__ __forceinline__ static int pad(int i) { return i + (i >> 4); }
-
+  
   __device__ void fail(int code) {
-    if (tid == 0 && sm.status == 0) sm.status = code;
+    if (tid == 0 && SMX.status == 0) SMX.status = code;
   }
 
   // ---- one pass over the N x M matrix (score_dual.cpp:25-49) ------------------------
   // PASS_EVAL : b_j = max_i (s_ji - alpha_i), arg = first max; counts; optional model_of.
   // PASS_FIXED: b_j = s_j,mo[j] (mo == null -> column 0).
-  // Result: sm.S = the reference's sequential FP64 sum of b_j, bit for bit.
+  // Result: SMX.S = the reference's sequential FP64 sum of b_j, bit for bit.
+  //
+  // Per tile of R = L*T rows:
+  //  phase 1 (coalesced, all threads): rows -> b_j into smem, argmax, packed counts.
+  //  phase 2 (all threads): thread t owns the contiguous chunk [t*L, t*L+L).  An
+  //    approximate block scan of (sum b, sum |b|) locates the binade of the running sum at
+  //    both chunk ends; a monotone chunk (all b >= 0 or all <= 0) whose two ends sit in
+  //    the same binade with margin E is SAFE and maps S -> S + u*Q_p (integer quanta,
+  //    two tracks for half-ulp ties).  Otherwise the chunk is RAW (exact IEEE adds).
+  //    A segmented warp scan composes runs of SAFE chunks of one binade into a single
+  //    piece, so each warp publishes ~1 piece (a few around binade crossings).
+  //  phase 3 (thread 0): apply the pieces in order to the exact running sum S.
+  static constexpr int LP = L | 1;  // odd chunk stride in smem: conflict-free chunk reads
+  __device__ __forceinline__ static int bpos(int k) { return (k / L) * LP + (k % L); }
+
+  // quanta of one |b| for u = 2^(base_sh - 1023 - 52): floor and half-way flag (exact, INT)
+  __device__ __forceinline__ static long long quanta_floor(double ab, int base_sh, bool& tie,
+                                                           bool& above) {
+    const unsigned long long B =
+        (unsigned long long)__double_as_longlong(ab) & 0x7fffffffffffffffull;
+    const int ebits = (int)(B >> 52);
+    const unsigned long long Mb =
+        (B & 0x000fffffffffffffull) | (ebits ? 0x0010000000000000ull : 0ull);
+    const int sh = base_sh - max(ebits, 1);
+    tie = false;
+    above = false;
+    if (sh <= 0) return (long long)(Mb << (-sh));
+    if (sh >= 54) return 0;
+    const unsigned long long rem = Mb & ((1ull << sh) - 1ull);
+    const unsigned long long half = 1ull << (sh - 1);
+    tie = (rem == half);
+    above = (rem > half);
+    return (long long)(Mb >> sh);
+  }
+
   __device__ void pass(int mode, const double* alpha_s, bool want_counts, uint8_t* mo_out,
                        const uint8_t* mo_in) {
-    __syncthreads();  // callers may still be reading the previous pass's sm.S / counts
+    if (mode == PASS_EVAL) {
+      if (m == MM) pass_t<PASS_EVAL, true>(n, alpha_s, want_counts, mo_out, mo_in);
+      else pass_t<PASS_EVAL, false>(n, alpha_s, want_counts, mo_out, mo_in);
+    } else {
+      pass_t<PASS_FIXED, false>(n, alpha_s, want_counts, mo_out, mo_in);
+    }
+  }
+
+  // Rows per load group in phase 1 (all loads of a group are in flight together).
+  static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : 2);
+  static_assert(L % G == 0, "L must be a multiple of the load group");
+
+  template <int MODE, bool FULLM>
+  __device__ __noinline__ void pass_t(const int n_, const double* alpha_s, const bool want_counts,
+                                      uint8_t* mo_out, const uint8_t* mo_in) {
+    const int tid_ = threadIdx.x, lane_ = tid_ & 31, wid_ = tid_ >> 5;
+    const int m_ = FULLM ? MM : jb.m;
+    const double* __restrict__ sc = jb.scores;
+    __syncthreads();  // callers may still be reading the previous pass's S / counts
     double a[MM];
 #pragma unroll
-    for (int i = 0; i < MM; ++i) a[i] = (i < m) ? alpha_s[i] : 0.0;
-    if (tid == 0) {
-      sm.S = 0.0;
-      sm.P = 0.0;
-      sm.A = 0.0;
-      if (mode == PASS_EVAL) sm.eval_passes++;
+    for (int i = 0; i < MM; ++i) a[i] = (FULLM || i < m_) ? alpha_s[i] : 0.0;
+    if (tid_ == 0) {
+      SMX.S = 0.0;
+      SMX.P = 0.0;
+      SMX.A = 0.0;
+      if (MODE == PASS_EVAL) SMX.eval_passes++;
     }
-    if (tid < MM) sm.counts[tid] = 0;
+    if (tid_ < MM) SMX.counts[tid_] = 0;
     __syncthreads();
-    const double* __restrict__ sc = jb.scores;
-    const bool vec2 = ((m & 1) == 0);
-    for (int base = 0; base < n; base += R) {
-      const int len = min(R, n - base);
-      // -- phase 1: coalesced rows -> b_j, argmax, packed counts -----------------------
+    const bool vec2 = FULLM ? (MM % 2 == 0) : ((m_ & 1) == 0);
+    for (int base = 0; base < n_; base += R) {
+      const int len = min(R, n_ - base);
+      // -- phase 1 ----------------------------------------------------------------------
+      long long t_p1 = clock64();
       unsigned long long pk[NPK];
 #pragma unroll
       for (int q = 0; q < NPK; ++q) pk[q] = 0ull;
-#pragma unroll 2
-      for (int r = 0; r < L; ++r) {
-        const int k = r * T + tid;
-        if (k < len) {
-          const int j = base + k;
-          const double* row = sc + (size_t)j * m;
-          double bj;
-          int arg;
-          if (mode == PASS_EVAL) {
-            double v[MM];
+      for (int r0 = 0; r0 < L; r0 += G) {
+        if (r0 * T >= len) break;  // block-uniform
+        double v[G][MODE == PASS_EVAL ? MM : 1];
+        int ag[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int kk = min((r0 + g) * T + tid_, len - 1);
+          const double* row = sc + (size_t)(base + kk) * m_;
+          if (MODE == PASS_EVAL) {
             if (vec2) {
               const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
               for (int i = 0; i < MM / 2; ++i) {
-                if (2 * i < m) {
-                  double2 x = __ldg(r2 + i);
-                  v[2 * i] = x.x;
-                  v[2 * i + 1] = x.y;
+                if (FULLM || 2 * i < m_) {
+                  const double2 x = __ldg(r2 + i);
+                  v[g][2 * i] = x.x;
+                  v[g][2 * i + 1] = x.y;
                 } else {
-                  v[2 * i] = 0.0;
-                  v[2 * i + 1] = 0.0;
+                  v[g][2 * i] = 0.0;
+                  v[g][2 * i + 1] = 0.0;
                 }
               }
             } else {
 #pragma unroll
-              for (int i = 0; i < MM; ++i) v[i] = (i < m) ? __ldg(row + i) : 0.0;
+              for (int i = 0; i < MM; ++i) v[g][i] = (FULLM || i < m_) ? __ldg(row + i) : 0.0;
             }
-            bj = __dsub_rn(v[0], a[0]);
+          } else {
+            ag[g] = mo_in ? (int)mo_in[base + kk] : 0;
+            v[g][0] = __ldg(row + ag[g]);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int k = (r0 + g) * T + tid_;
+          double bj;
+          int arg;
+          if (MODE == PASS_EVAL) {
+            bj = __dsub_rn(v[g][0], a[0]);
             arg = 0;
 #pragma unroll
             for (int i = 1; i < MM; ++i) {
-              if (i < m) {
-                double x = __dsub_rn(v[i], a[i]);
+              if (FULLM || i < m_) {
+                const double x = __dsub_rn(v[g][i], a[i]);
                 if (x > bj) {
                   bj = x;
                   arg = i;
@@ -305,16 +377,22 @@ struct Solver {
               }
             }
           } else {
-            arg = mo_in ? (int)mo_in[j] : 0;
-            bj = __ldg(row + arg);
+            bj = v[g][0];
+            arg = ag[g];
           }
-          sm.b[pad(k)] = bj;
-          if (want_counts) {
+          if (k < len) {
+            SMX.b[bpos(k)] = bj;
+            if (want_counts) {
+              if (NPK == 1) {
+                pk[0] += 1ull << (arg * 16);
+              } else {
 #pragma unroll
-            for (int q = 0; q < NPK; ++q)
-              pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+                for (int q = 0; q < NPK; ++q)
+                  pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+              }
+            }
+            if (mo_out) mo_out[base + k] = (uint8_t)arg;
           }
-          if (mo_out) mo_out[j] = (uint8_t)arg;
         }
       }
       if (want_counts) {
@@ -323,163 +401,221 @@ struct Solver {
           unsigned long long x = pk[q];
 #pragma unroll
           for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
-          if (lane == 0) {
+          if (lane_ == 0) {
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-              int i = 4 * q + f;
-              unsigned cnt = (unsigned)((x >> (16 * f)) & 0xffffull);
-              if (i < m && cnt) atomicAdd(&sm.counts[i], (int)cnt);
+              const int i = 4 * q + f;
+              const unsigned cnt = (unsigned)((x >> (16 * f)) & 0xffffull);
+              if (i < m_ && cnt) atomicAdd(&SMX.counts[i], (int)cnt);
             }
           }
         }
       }
       __syncthreads();
-      // -- phase 2: chunk quanta --------------------------------------------------------
-      const int c0 = tid * L;
+      long long t_p2 = clock64();
+      if (tid_ == 0) SMX.prof[0] += t_p2 - t_p1;
+      // -- phase 2 ----------------------------------------------------------------------
+      const int c0 = tid_ * L;
       const int cnt = max(0, min(L, len - c0));
-      double bl[L];
-      double ps = 0.0, pa = 0.0;
+      const double* bch = SMX.b + tid_ * LP;
+      double ps = 0.0;
+      unsigned orhi = 0u, andhi = 0xffffffffu;
 #pragma unroll
       for (int r = 0; r < L; ++r) {
-        bl[r] = (r < cnt) ? sm.b[pad(c0 + r)] : 0.0;
-        ps += bl[r];
-        pa += fabs(bl[r]);
+        if (r < cnt) {
+          const double x = bch[r];
+          ps += x;
+          const unsigned hi = (unsigned)__double2hiint(x);
+          orhi |= hi;
+          andhi &= hi;
+        }
       }
-      // block exclusive scan of (ps, pa) (approximate: only used with an error margin)
+      const bool allpos = (orhi >> 31) == 0u;    // every b has its sign bit clear (incl. +0)
+      const bool allneg = (andhi >> 31) != 0u;   // every b has its sign bit set
+      double pa;
+      if (allpos) pa = ps;
+      else if (allneg) pa = -ps;
+      else {
+        pa = 0.0;
+#pragma unroll
+        for (int r = 0; r < L; ++r)
+          if (r < cnt) pa += fabs(bch[r]);
+      }
+      // block exclusive scan of (ps, pa) — approximate; used only behind a margin
       double ix = ps, iy = pa;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         double tx = __shfl_up_sync(FULL, ix, off), ty = __shfl_up_sync(FULL, iy, off);
-        if (lane >= off) {
+        if (lane_ >= off) {
           ix += tx;
           iy += ty;
         }
       }
-      if (lane == 31) {
-        sm.scan_x[wid] = ix;
-        sm.scan_y[wid] = iy;
+      if (lane_ == 31) {
+        SMX.scan_x[wid_] = ix;
+        SMX.scan_y[wid_] = iy;
+      }
+      __syncthreads();
+      if (wid_ == 0) {  // exclusive scan of the W warp totals (+ the tile carry)
+        double wx = (lane_ < W) ? SMX.scan_x[lane_] : 0.0;
+        double wy = (lane_ < W) ? SMX.scan_y[lane_] : 0.0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          double tx = __shfl_up_sync(FULL, wx, off), ty = __shfl_up_sync(FULL, wy, off);
+          if (lane_ >= off) {
+            wx += tx;
+            wy += ty;
+          }
+        }
+        const double ox = __shfl_up_sync(FULL, wx, 1), oy = __shfl_up_sync(FULL, wy, 1);
+        const double cp = SMX.P, ca = SMX.A;
+        if (lane_ < W) {
+          SMX.scan_x[lane_] = cp + (lane_ ? ox : 0.0);
+          SMX.scan_y[lane_] = ca + (lane_ ? oy : 0.0);
+        }
+        if (lane_ == W - 1) {
+          SMX.tileP = wx;
+          SMX.tileA = wy;
+        }
       }
       double ex = __shfl_up_sync(FULL, ix, 1), ey = __shfl_up_sync(FULL, iy, 1);
-      if (lane == 0) {
+      if (lane_ == 0) {
         ex = 0.0;
         ey = 0.0;
       }
       __syncthreads();
-      double wx = 0.0, wy = 0.0, tx = 0.0, ty = 0.0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        double sx = sm.scan_x[w], sy = sm.scan_y[w];
-        if (w < wid) {
-          wx += sx;
-          wy += sy;
-        }
-        tx += sx;
-        ty += sy;
-      }
-      double P = sm.P + (wx + ex);
-      double A = sm.A + (wy + ey);
+      const double P0 = SMX.scan_x[wid_] + ex;
+      const double A0 = SMX.scan_y[wid_] + ey;
       const long long jg = (long long)base + c0;
-      int safe = cnt > 0;
+      int kind = (cnt > 0) ? PIECE_RAW : PIECE_NONE;
       int e_ref = 0, neg_ref = 0;
-#pragma unroll
-      for (int r = 0; r <= L; ++r) {
-        if (r <= cnt && safe) {
-          double Ab = A + ((r < cnt) ? fabs(bl[r]) : 0.0);
-          double E = (double)(jg + r + 64) * 0x1p-51 * Ab;
-          int e, ng;
-          if (!in_binade(P, E, e, ng)) safe = 0;
-          else if (r == 0) {
-            e_ref = e;
-            neg_ref = ng;
-          } else if (e != e_ref || ng != neg_ref) safe = 0;
-        }
-        if (r < cnt) {
-          P += bl[r];
-          A += fabs(bl[r]);
+      if (cnt > 0) {
+        if (allpos || allneg) {
+          // S_j is monotone across the chunk: both ends in one binade => all inside.
+          const double P1 = P0 + ps, A1 = A0 + pa;
+          const double E = (double)(jg + cnt + 64) * 0x1p-51 * A1;
+          int e1, n1;
+          if (in_binade(P0, E, e_ref, neg_ref) && in_binade(P1, E, e1, n1) && e1 == e_ref &&
+              n1 == neg_ref)
+            kind = PIECE_SAFE;
+        } else {
+          double P = P0, A = A0;
+          bool ok = true;
+          for (int r = 0; r <= cnt && ok; ++r) {
+            const double x = (r < cnt) ? bch[r] : 0.0;
+            const double E = (double)(jg + r + 64) * 0x1p-51 * (A + fabs(x));
+            int e, ng;
+            if (!in_binade(P, E, e, ng)) ok = false;
+            else if (r == 0) {
+              e_ref = e;
+              neg_ref = ng;
+            } else if (e != e_ref || ng != neg_ref) ok = false;
+            P += x;
+            A += fabs(x);
+          }
+          if (ok) kind = PIECE_SAFE;
         }
       }
       long long Q0 = 0, Q1 = 0;
-      if (safe) {
-        const double scale = __longlong_as_double((long long)(52 - e_ref + 1023) << 52);
+      if (kind == PIECE_SAFE) {
+        // q_j = round(b_j / u) with u = 2^(e-52): exact integer quanta of each b_j
+        const int base_sh = 1023 + e_ref;
+        bool tie_any = false;
+        if (allpos) {
 #pragma unroll
-        for (int r = 0; r < L; ++r) {
-          if (r < cnt) {
-            double y = bl[r] * scale;  // exact (power-of-two scaling)
-            double fy = floor(y);
-            double fr = y - fy;        // exact
-            long long qf = (long long)fy;
-            if (fr == 0.5) {  // half-ulp tie: RNE to the even result
-              Q0 += ((Q0 + qf) & 1) ? qf + 1 : qf;
-              Q1 += ((1 + Q1 + qf) & 1) ? qf + 1 : qf;
+          for (int r = 0; r < L; ++r) {
+            if (r < cnt) {
+              bool tie, above;
+              long long q = quanta_floor(bch[r], base_sh, tie, above);
+              Q0 += q + (above ? 1 : 0);
+              tie_any |= tie;
+            }
+          }
+          Q1 = Q0;
+        }
+        if (!allpos || tie_any) {  // general: signed b, two parity tracks for ties
+          Q0 = 0;
+          Q1 = 0;
+          for (int r = 0; r < cnt; ++r) {
+            const double x = bch[r];
+            bool tie, above;
+            long long q = quanta_floor(x, base_sh, tie, above);
+            const bool negb = x < 0.0;
+            if (tie) {  // |x|/u = q + 1/2; RNE picks the neighbour leaving S/u even
+              const long long lo = negb ? -q - 1 : q;
+              Q0 += ((Q0 + lo) & 1) ? lo + 1 : lo;
+              Q1 += ((1 + Q1 + lo) & 1) ? lo + 1 : lo;
             } else {
-              long long q = (fr > 0.5) ? qf + 1 : qf;
-              Q0 += q;
-              Q1 += q;
+              const long long qq = q + (above ? 1 : 0);
+              Q0 += negb ? -qq : qq;
+              Q1 += negb ? -qq : qq;
             }
           }
         }
       }
-      sm.q0[tid] = Q0;
-      sm.q1[tid] = Q1;
-      sm.safe[tid] = (unsigned char)safe;
-      const int key = safe ? (e_ref * 2 + neg_ref) : (100000 + lane);
-      const bool uni = __all_sync(FULL, key == __shfl_sync(FULL, key, 0));
-      if (uni) {  // ordered tree composition of the 32 chunk maps
+      // segmented warp scan: compose consecutive SAFE chunks of one binade
+      const int key = (kind == PIECE_SAFE) ? (e_ref * 2 + neg_ref) : -100000 - lane_;
+      const int pkey = __shfl_up_sync(FULL, key, 1);
+      const bool head = (lane_ == 0) || kind != PIECE_SAFE || pkey != key;
+      {
+        bool f = head;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          long long o0 = __shfl_down_sync(FULL, Q0, d), o1 = __shfl_down_sync(FULL, Q1, d);
-          if ((lane & (2 * d - 1)) == 0) {
-            long long n0 = Q0 + ((Q0 & 1) ? o1 : o0);
-            long long n1 = Q1 + (((1 + Q1) & 1) ? o1 : o0);
+          long long o0 = __shfl_up_sync(FULL, Q0, d), o1 = __shfl_up_sync(FULL, Q1, d);
+          bool of = __shfl_up_sync(FULL, f, d);
+          if (lane_ >= d && !f) {
+            long long n0 = o0 + ((o0 & 1) ? Q1 : Q0);
+            long long n1 = o1 + (((1 + o1) & 1) ? Q1 : Q0);
             Q0 = n0;
             Q1 = n1;
+            f = of;
           }
         }
       }
-      if (lane == 0) {
-        sm.wuni[wid] = uni ? 1 : 0;
-        sm.wq0[wid] = Q0;
-        sm.wq1[wid] = Q1;
-        if (wid == 0) {
-          sm.tileP = tx;
-          sm.tileA = ty;
-        }
+      const bool nhead = __shfl_down_sync(FULL, head, 1);
+      const bool tail = (kind != PIECE_NONE) && (lane_ == 31 || nhead);
+      const unsigned tmask = __ballot_sync(FULL, tail);
+      if (tail) {
+        const int slot = wid_ * 32 + __popc(tmask & ((1u << lane_) - 1u));
+        SMX.pkind[slot] = (unsigned char)kind;
+        SMX.q0[slot] = (kind == PIECE_SAFE) ? Q0 : (long long)(tid_ * LP);
+        SMX.q1[slot] = (kind == PIECE_SAFE) ? Q1 : (long long)cnt;
       }
+      if (lane_ == 0) SMX.wcnt[wid_] = __popc(tmask);
       __syncthreads();
-      // -- phase 3: ordered walk (one thread) -------------------------------------------
-      if (tid == 0) {
-        double S = sm.S;
-        const int nw = min(W, (len + 32 * L - 1) / (32 * L));
-        for (int w = 0; w < nw; ++w) {
-          if (sm.wuni[w]) {
-            S = apply_quanta(S, sm.wq0[w], sm.wq1[w]);
-            continue;
-          }
-          for (int l = 0; l < 32; ++l) {
-            const int t = w * 32 + l;
-            const int tc0 = t * L;
-            const int tcnt = min(L, len - tc0);
-            if (tcnt <= 0) break;
-            if (sm.safe[t]) {
-              S = apply_quanta(S, sm.q0[t], sm.q1[t]);
+      long long t_p3 = clock64();
+      if (tid_ == 0) SMX.prof[1] += t_p3 - t_p2;
+      // -- phase 3: ordered walk over the pieces (one thread) ----------------------------
+      if (tid_ == 0) {
+        double S = SMX.S;
+        for (int w = 0; w < W; ++w) {
+          const int np = SMX.wcnt[w];
+          for (int p = 0; p < np; ++p) {
+            const int slot = w * 32 + p;
+            const long long x0 = SMX.q0[slot], x1 = SMX.q1[slot];
+            if (SMX.pkind[slot] == PIECE_SAFE) {
+              S = apply_quanta(S, x0, x1);
             } else {
-              for (int r = 0; r < tcnt; ++r) S = __dadd_rn(S, sm.b[pad(tc0 + r)]);
+              const double* rb = SMX.b + (int)x0;
+              const int rc = (int)x1;
+              for (int r = 0; r < rc; ++r) S = __dadd_rn(S, rb[r]);
             }
           }
         }
-        sm.S = S;
-        sm.P += sm.tileP;
-        sm.A += sm.tileA;
+        SMX.S = S;
+        SMX.P += SMX.tileP;
+        SMX.A += SMX.tileA;
       }
       __syncthreads();
+      if (tid_ == 0) SMX.prof[2] += clock64() - t_p3;
     }
   }
 
   // g(alpha) = (sum_j best_j + sum_i alpha_i c_i) / N   (score_dual.cpp:47-48)
   __device__ double eval_dual(const double* alpha_s, bool want_counts, uint8_t* mo_out) {
     pass(PASS_EVAL, alpha_s, want_counts, mo_out, nullptr);
-    double g = sm.S;
-    for (int i = 0; i < m; ++i) g = __dadd_rn(g, __dmul_rn(alpha_s[i], sm.c[i]));
+    double g = SMX.S;
+    for (int i = 0; i < m; ++i) g = __dadd_rn(g, __dmul_rn(alpha_s[i], SMX.c[i]));
     return __ddiv_rn(g, (double)n);  // every thread computes the same value
   }
 
@@ -488,7 +624,7 @@ struct Solver {
     unsigned act = __activemask();
     unsigned key = ok ? d : 0xffffffffu;
     unsigned peers = __match_any_sync(act, key);
-    if (ok && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[d], __popc(peers));
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(&SMX.hist[d], __popc(peers));
   }
   // Picks the digit holding the sel_k-th largest among counted candidates (warp 0).
   __device__ void select_digit(int shift) {
@@ -497,7 +633,7 @@ struct Solver {
       const int top = 255 - 8 * lane;
       int local = 0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) local += (int)sm.hist[top - q];
+      for (int q = 0; q < 8; ++q) local += (int)SMX.hist[top - q];
       int incl = local;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -505,14 +641,14 @@ struct Solver {
         if (lane >= off) incl += t;
       }
       const int excl = incl - local;
-      const int k = sm.sel_k;
+      const int k = SMX.sel_k;
       if (excl < k && k <= incl) {
         int above = excl;
         for (int q = 0; q < 8; ++q) {
-          int h = (int)sm.hist[top - q];
+          int h = (int)SMX.hist[top - q];
           if (above + h >= k) {
-            sm.sel_prefix |= (unsigned long long)(top - q) << shift;
-            sm.sel_k = k - above;
+            SMX.sel_prefix |= (unsigned long long)(top - q) << shift;
+            SMX.sel_k = k - above;
             break;
           }
           above += h;
@@ -521,26 +657,41 @@ struct Solver {
     }
   }
 
-  // ---- polish_pass (score_dual.cpp:54-76) on sm.polished --------------------------------
-  __device__ void polish_pass() {
+  // ---- polish_pass (score_dual.cpp:54-76) on SMX.polished --------------------------------
+  // For coordinate i the new price is the k-th largest b_j = s_ji - max_{k!=i}(s_jk - a_k),
+  // k = ceil(c_i - 1e-9) (nth_element, :69-72).  Near the optimum that value sits close to
+  // the current a_i, so one sweep counts the keys above a window [a_i - d, a_i + d] and
+  // gathers the keys inside it into shared memory; the k-th largest is then selected among
+  // the few candidates (radix select in smem).  If the window misses or overflows, an exact
+  // 8-digit radix select over all N keys (written during the same sweep) is the fallback.
+  // d adapts per CTA; the result is exact either way.
+  __device__ __noinline__ void polish_pass() {
+    constexpr int CAP = SM::BPAD;
+    const long long t_pol = clock64();
     if (tid == 0) {
-      sm.max_delta = 0.0;
-      sm.polish_passes++;
+      SMX.max_delta = 0.0;
+      SMX.polish_passes++;
     }
+    unsigned long long* cand = reinterpret_cast<unsigned long long*>(SMX.b);
     for (int i = 0; i < m; ++i) {
       __syncthreads();
       double a[MM];
 #pragma unroll
-      for (int q = 0; q < MM; ++q) a[q] = (q < m) ? sm.polished[q] : 0.0;
-      const double ci = sm.c[i];
+      for (int q = 0; q < MM; ++q) a[q] = (q < m) ? SMX.polished[q] : 0.0;
+      const double ci = SMX.c[i];
       int k = ci > 1e-12 ? (int)ceil(__dsub_rn(ci, 1e-9)) : 1;
       k = max(1, min(k, n));
-      if (tid < 256) sm.hist[tid] = 0u;
+      const double ai = SMX.polished[i], dl = SMX.pol_delta;
+      const unsigned long long klo = dkey(ai - dl), khi = dkey(ai + dl);
+      if (tid < 256) SMX.hist[tid] = 0u;
       if (tid == 0) {
-        sm.sel_prefix = 0ull;
-        sm.sel_k = k;
+        SMX.sel_prefix = 0ull;
+        SMX.sel_k = k;
+        SMX.cand_n = 0;
+        SMX.above_n = 0;
       }
       __syncthreads();
+      int my_above = 0;
       for (int j = tid; j < n; j += T) {
         const double* row = jb.scores + (size_t)j * m;
         double rest = -CUDART_INF;
@@ -553,32 +704,72 @@ struct Solver {
             else rest = smax(rest, __dsub_rn(v, a[q]));
           }
         }
-        unsigned long long key = dkey(__dsub_rn(vi, rest));
+        const unsigned long long key = dkey(__dsub_rn(vi, rest));
         keys[j] = key;
-        hist_add(true, (unsigned)(key >> 56));
-      }
-      __syncthreads();
-      select_digit(56);
-      for (int shift = 48; shift >= 0; shift -= 8) {
-        __syncthreads();
-        if (tid < 256) sm.hist[tid] = 0u;
-        __syncthreads();
-        const unsigned long long hi = sm.sel_prefix >> (shift + 8);
-        for (int j = tid; j < n; j += T) {
-          unsigned long long key = keys[j];
-          hist_add((key >> (shift + 8)) == hi, (unsigned)((key >> shift) & 0xffull));
+        my_above += (key > khi) ? 1 : 0;
+        const bool in = (key >= klo) && (key <= khi);
+        const unsigned act = __activemask();
+        const unsigned inm = __ballot_sync(act, in);
+        if (inm) {
+          const int leader = __ffs(inm) - 1;
+          int basepos = 0;
+          if (lane == leader) basepos = atomicAdd(&SMX.cand_n, __popc(inm));
+          basepos = __shfl_sync(act, basepos, leader);
+          if (in) {
+            const int pos = basepos + __popc(inm & ((1u << lane) - 1u));
+            if (pos < CAP) cand[pos] = key;
+          }
         }
-        __syncthreads();
-        select_digit(shift);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) my_above += __shfl_down_sync(FULL, my_above, off);
+      if (lane == 0 && my_above) atomicAdd(&SMX.above_n, my_above);
+      __syncthreads();
+      const int nc = SMX.cand_n, na = SMX.above_n;
+      const bool win = (nc <= CAP) && (na < k) && (k <= na + nc);
+      if (win) {
+        if (tid == 0) SMX.sel_k = k - na;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          __syncthreads();
+          if (tid < 256) SMX.hist[tid] = 0u;
+          __syncthreads();
+          const unsigned long long hi = (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8));
+          for (int q = tid; q < nc; q += T) {
+            const unsigned long long key = cand[q];
+            hist_add(shift == 56 || (key >> (shift + 8)) == hi,
+                     (unsigned)((key >> shift) & 0xffull));
+          }
+          __syncthreads();
+          select_digit(shift);
+        }
+      } else {
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          __syncthreads();
+          if (tid < 256) SMX.hist[tid] = 0u;
+          __syncthreads();
+          const unsigned long long hi = (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8));
+          for (int j = tid; j < n; j += T) {
+            const unsigned long long key = keys[j];
+            hist_add(shift == 56 || (key >> (shift + 8)) == hi,
+                     (unsigned)((key >> shift) & 0xffull));
+          }
+          __syncthreads();
+          select_digit(shift);
+        }
       }
       __syncthreads();
       if (tid == 0) {
-        double next = dkey_inv(sm.sel_prefix);
-        sm.max_delta = smax(sm.max_delta, fabs(__dsub_rn(next, sm.polished[i])));
-        sm.polished[i] = next;
+        const double next = dkey_inv(SMX.sel_prefix);
+        SMX.max_delta = smax(SMX.max_delta, fabs(__dsub_rn(next, SMX.polished[i])));
+        SMX.polished[i] = next;
+        if (nc > CAP) SMX.pol_delta *= 0.125;
+        else if (!win) SMX.pol_delta = fmin(SMX.pol_delta * 8.0, 4.0);
+        else if (nc > CAP / 4) SMX.pol_delta *= 0.5;
+        if (!win) SMX.prof[4]++;
       }
     }
     __syncthreads();
+    if (tid == 0) SMX.prof[3] += clock64() - t_pol;
   }
 
   // ---- block argmin / argmax helpers (lexicographic with index tie-break) ------------
@@ -596,27 +787,27 @@ struct Solver {
       }
     }
     if (lane == 0) {
-      sm.red_d[wid] = val;
-      sm.red_j[wid] = j;
-      sm.red_v[wid] = v;
+      SMX.red_d[wid] = val;
+      SMX.red_j[wid] = j;
+      SMX.red_v[wid] = v;
     }
     __syncthreads();
     if (tid == 0) {
       for (int w = 1; w < W; ++w) {
-        double ov = sm.red_d[w];
-        int oj = sm.red_j[w];
-        if (oj >= 0 && (sm.red_j[0] < 0 || ov < sm.red_d[0] ||
-                        (ov == sm.red_d[0] && oj < sm.red_j[0]))) {
-          sm.red_d[0] = ov;
-          sm.red_j[0] = oj;
-          sm.red_v[0] = sm.red_v[w];
+        double ov = SMX.red_d[w];
+        int oj = SMX.red_j[w];
+        if (oj >= 0 && (SMX.red_j[0] < 0 || ov < SMX.red_d[0] ||
+                        (ov == SMX.red_d[0] && oj < SMX.red_j[0]))) {
+          SMX.red_d[0] = ov;
+          SMX.red_j[0] = oj;
+          SMX.red_v[0] = SMX.red_v[w];
         }
       }
     }
     __syncthreads();
-    val = sm.red_d[0];
-    j = sm.red_j[0];
-    v = sm.red_v[0];
+    val = SMX.red_d[0];
+    j = SMX.red_j[0];
+    v = SMX.red_v[0];
     __syncthreads();
   }
   __device__ void block_argmax(double& val, int& j) {
@@ -631,48 +822,48 @@ struct Solver {
       }
     }
     if (lane == 0) {
-      sm.red_d[wid] = val;
-      sm.red_j[wid] = j;
+      SMX.red_d[wid] = val;
+      SMX.red_j[wid] = j;
     }
     __syncthreads();
     if (tid == 0) {
       for (int w = 1; w < W; ++w) {
-        double ov = sm.red_d[w];
-        int oj = sm.red_j[w];
-        if (oj >= 0 && (sm.red_j[0] < 0 || ov > sm.red_d[0] ||
-                        (ov == sm.red_d[0] && oj < sm.red_j[0]))) {
-          sm.red_d[0] = ov;
-          sm.red_j[0] = oj;
+        double ov = SMX.red_d[w];
+        int oj = SMX.red_j[w];
+        if (oj >= 0 && (SMX.red_j[0] < 0 || ov > SMX.red_d[0] ||
+                        (ov == SMX.red_d[0] && oj < SMX.red_j[0]))) {
+          SMX.red_d[0] = ov;
+          SMX.red_j[0] = oj;
         }
       }
     }
     __syncthreads();
-    val = sm.red_d[0];
-    j = sm.red_j[0];
+    val = SMX.red_d[0];
+    j = SMX.red_j[0];
     __syncthreads();
   }
 
-  // ---- repair_counts (score_dual.cpp:81-185); counts in sm.counts, targets in sm.target
+  // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
     if (tid == 0) {
-      sm.repair_calls++;
-      for (int i = 0; i < m; ++i) sm.delta[i] = sm.counts[i] - sm.target[i];
+      SMX.repair_calls++;
+      for (int i = 0; i < m; ++i) SMX.delta[i] = SMX.counts[i] - SMX.target[i];
     }
     __syncthreads();
     // Phase 1: min-loss single moves while any surplus remains (:96-118)
     for (;;) {
       bool over = false;
-      for (int i = 0; i < m; ++i) over = over || sm.delta[i] > 0;
+      for (int i = 0; i < m; ++i) over = over || SMX.delta[i] > 0;
       if (!over) break;
       double bl = CUDART_INF;
       int bj = -1, bv = -1;
       for (int j = tid; j < n; j += T) {
         int u = mo[j];
-        if (sm.delta[u] <= 0) continue;
+        if (SMX.delta[u] <= 0) continue;
         const double* row = jb.scores + (size_t)j * m;
         double su = __ldg(row + u);
         for (int v = 0; v < m; ++v) {
-          if (sm.delta[v] >= 0) continue;
+          if (SMX.delta[v] >= 0) continue;
           double loss = __dsub_rn(su, __ldg(row + v));
           if (bj < 0 || loss < bl) {
             bl = loss;
@@ -685,10 +876,10 @@ struct Solver {
       if (tid == 0) {
         int u = mo[bj];
         mo[bj] = (uint8_t)bv;
-        sm.counts[u]--;
-        sm.counts[bv]++;
-        sm.delta[u]--;
-        sm.delta[bv]++;
+        SMX.counts[u]--;
+        SMX.counts[bv]++;
+        SMX.delta[u]--;
+        SMX.delta[bv]++;
       }
       __syncthreads();
     }
@@ -723,8 +914,8 @@ struct Solver {
             int j = bjv[v];
             block_argmax(g, j);
             if (tid == 0) {
-              sm.gain[u * m + v] = (j >= 0) ? g : -CUDART_INF;
-              sm.witness[u * m + v] = j;
+              SMX.gain[u * m + v] = (j >= 0) ? g : -CUDART_INF;
+              SMX.witness[u * m + v] = j;
             }
           }
         }
@@ -734,7 +925,7 @@ struct Solver {
           int cu = -1, cv = -1, cw = -1;
           for (int u = 0; u < m; ++u)
             for (int v = u + 1; v < m; ++v) {
-              double g = __dadd_rn(sm.gain[u * m + v], sm.gain[v * m + u]);
+              double g = __dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + u]);
               if (g > best) {
                 best = g;
                 cu = u;
@@ -747,8 +938,8 @@ struct Solver {
               if (v == u) continue;
               for (int w = 0; w < m; ++w) {
                 if (w == u || w == v) continue;
-                double g = __dadd_rn(__dadd_rn(sm.gain[u * m + v], sm.gain[v * m + w]),
-                                     sm.gain[w * m + u]);
+                double g = __dadd_rn(__dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + w]),
+                                     SMX.gain[w * m + u]);
                 if (g > best) {
                   best = g;
                   cu = u;
@@ -757,23 +948,23 @@ struct Solver {
                 }
               }
             }
-          sm.flag = (cu < 0);
+          SMX.flag = (cu < 0);
           if (cu >= 0) {
             auto move = [&](int j, int v) {
               int uu = mo[j];
               mo[j] = (uint8_t)v;
-              sm.counts[uu]--;
-              sm.counts[v]++;
-              sm.delta[uu]--;
-              sm.delta[v]++;
+              SMX.counts[uu]--;
+              SMX.counts[v]++;
+              SMX.delta[uu]--;
+              SMX.delta[v]++;
             };
             if (cw < 0) {
-              int j1 = sm.witness[cu * m + cv], j2 = sm.witness[cv * m + cu];
+              int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cu];
               move(j1, cv);
               move(j2, cu);
             } else {
-              int j1 = sm.witness[cu * m + cv], j2 = sm.witness[cv * m + cw],
-                  j3 = sm.witness[cw * m + cu];
+              int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cw],
+                  j3 = SMX.witness[cw * m + cu];
               move(j1, cv);
               move(j2, cw);
               move(j3, cu);
@@ -781,212 +972,212 @@ struct Solver {
           }
         }
         __syncthreads();
-        if (sm.flag) break;
+        if (SMX.flag) break;
         __syncthreads();
       }
     }
     __syncthreads();
     // exact sequential mean of the repaired assignment (:182-184)
-    pass(PASS_FIXED, sm.zero, false, nullptr, mo);
-    return __ddiv_rn(sm.S, (double)n);
+    pass(PASS_FIXED, SMX.zero, false, nullptr, mo);
+    return __ddiv_rn(SMX.S, (double)n);
   }
 
   // ---- solve_dual (score_dual.cpp:232-327) ---------------------------------------------
-  // in: sm.c (targets), sm.init (when has_init); out: sm.alpha_star, score, dual_bound, gap,
-  // resid, iterations, converged, sm.counts (realised), mo (assignment)
+  // in: SMX.c (targets), SMX.init (when has_init); out: SMX.alpha_star, score, dual_bound, gap,
+  // resid, iterations, converged, SMX.counts (realised), mo (assignment)
   __device__ void solve_dual(const rw_subgradient_params& p, bool has_init) {
     if (tid == 0) {  // TargetCounts::validate (:195-205)
       double t = 0.0;
       bool ok = true;
       for (int i = 0; i < m; ++i) {
-        if (!isfinite(sm.c[i]) || sm.c[i] < -1e-9) ok = false;
-        t = __dadd_rn(t, sm.c[i]);
+        if (!isfinite(SMX.c[i]) || SMX.c[i] < -1e-9) ok = false;
+        t = __dadd_rn(t, SMX.c[i]);
       }
       double scale = (double)n > 1.0 ? (double)n : 1.0;
       if (!(fabs(__dsub_rn(t, (double)n)) <= __dmul_rn(1e-6, scale))) ok = false;
-      if (!ok && sm.status == 0) sm.status = RW_ERR_VALIDATION;
+      if (!ok && SMX.status == 0) SMX.status = RW_ERR_VALIDATION;
     }
     __syncthreads();
-    if (sm.status) return;
+    if (SMX.status) return;
     if (m == 1) {  // :239-249
-      pass(PASS_FIXED, sm.zero, false, nullptr, nullptr);
+      pass(PASS_FIXED, SMX.zero, false, nullptr, nullptr);
       for (int j = tid; j < n; j += T) mo[j] = 0;
       if (tid == 0) {
-        sm.alpha_star[0] = 0.0;
-        sm.score = sm.dual_bound = __ddiv_rn(sm.S, (double)n);
-        sm.gap = 0.0;
-        sm.resid[0] = __ddiv_rn(__dsub_rn((double)n, sm.c[0]), (double)n);
-        sm.counts[0] = n;
-        sm.iterations = 0;
-        sm.converged = 1;
+        SMX.alpha_star[0] = 0.0;
+        SMX.score = SMX.dual_bound = __ddiv_rn(SMX.S, (double)n);
+        SMX.gap = 0.0;
+        SMX.resid[0] = __ddiv_rn(__dsub_rn((double)n, SMX.c[0]), (double)n);
+        SMX.counts[0] = n;
+        SMX.iterations = 0;
+        SMX.converged = 1;
       }
       __syncthreads();
       return;
     }
     if (tid == 0) {
       for (int i = 0; i < m; ++i) {
-        sm.alpha[i] = has_init ? sm.init[i] : 0.0;
-        sm.best_alpha[i] = sm.alpha[i];
-        sm.zero[i] = 0.0;
+        SMX.alpha[i] = has_init ? SMX.init[i] : 0.0;
+        SMX.best_alpha[i] = SMX.alpha[i];
+        SMX.zero[i] = 0.0;
       }
-      sm.best_g = CUDART_INF;
-      sm.converged = 0;
-      sm.iterations = 0;
+      SMX.best_g = CUDART_INF;
+      SMX.converged = 0;
+      SMX.iterations = 0;
     }
     __syncthreads();
     {  // consider(0, g(0))  (:271-274)
-      double g = eval_dual(sm.zero, false, nullptr);
-      if (tid == 0 && g < sm.best_g) {
-        sm.best_g = g;
-        for (int i = 0; i < m; ++i) sm.best_alpha[i] = 0.0;
+      double g = eval_dual(SMX.zero, false, nullptr);
+      if (tid == 0 && g < SMX.best_g) {
+        SMX.best_g = g;
+        for (int i = 0; i < m; ++i) SMX.best_alpha[i] = 0.0;
       }
     }
     for (int t = 0; t < p.max_iters; ++t) {  // :279-292
-      double g = eval_dual(sm.alpha, true, nullptr);
+      double g = eval_dual(SMX.alpha, true, nullptr);
       if (tid == 0) {
-        if (g < sm.best_g) {
-          sm.best_g = g;
-          for (int i = 0; i < m; ++i) sm.best_alpha[i] = sm.alpha[i];
+        if (g < SMX.best_g) {
+          SMX.best_g = g;
+          for (int i = 0; i < m; ++i) SMX.best_alpha[i] = SMX.alpha[i];
         }
-        sm.iterations = t + 1;
+        SMX.iterations = t + 1;
         double resid = 0.0;
         for (int i = 0; i < m; ++i)
-          resid = smax(resid, fabs(__dsub_rn((double)sm.counts[i], sm.c[i])));
+          resid = smax(resid, fabs(__dsub_rn((double)SMX.counts[i], SMX.c[i])));
         resid = __ddiv_rn(resid, (double)n);
         if (resid <= p.residual_tol) {
-          sm.converged = 1;
-          sm.flag = 1;
+          SMX.converged = 1;
+          SMX.flag = 1;
         } else {
-          sm.flag = 0;
+          SMX.flag = 0;
           double eta = __ddiv_rn(p.eta0, sqrt(__dadd_rn((double)t, 1.0)));
           for (int i = 0; i < m; ++i)
-            sm.alpha[i] = __dadd_rn(
-                sm.alpha[i],
-                __ddiv_rn(__dmul_rn(eta, __dsub_rn((double)sm.counts[i], sm.c[i])), (double)n));
+            SMX.alpha[i] = __dadd_rn(
+                SMX.alpha[i],
+                __ddiv_rn(__dmul_rn(eta, __dsub_rn((double)SMX.counts[i], SMX.c[i])), (double)n));
         }
       }
       __syncthreads();
-      if (sm.flag) break;
+      if (SMX.flag) break;
     }
     if (tid == 0)
-      for (int i = 0; i < m; ++i) sm.polished[i] = sm.best_alpha[i];
+      for (int i = 0; i < m; ++i) SMX.polished[i] = SMX.best_alpha[i];
     for (int ps = 0; ps < p.polish_passes; ++ps) {  // :297-306
       polish_pass();
-      double g = eval_dual(sm.polished, false, nullptr);
+      double g = eval_dual(SMX.polished, false, nullptr);
       if (tid == 0) {
-        if (g < sm.best_g) {
-          sm.best_g = g;
-          for (int i = 0; i < m; ++i) sm.best_alpha[i] = sm.polished[i];
+        if (g < SMX.best_g) {
+          SMX.best_g = g;
+          for (int i = 0; i < m; ++i) SMX.best_alpha[i] = SMX.polished[i];
         }
-        sm.flag = (sm.max_delta <= 1e-15);
-        if (sm.flag) sm.converged = 1;
+        SMX.flag = (SMX.max_delta <= 1e-15);
+        if (SMX.flag) SMX.converged = 1;
       }
       __syncthreads();
-      if (sm.flag) break;
+      if (SMX.flag) break;
     }
     if (tid == 0) {  // gauge (:309-310)
-      double lo = sm.best_alpha[0];
+      double lo = SMX.best_alpha[0];
       for (int i = 1; i < m; ++i)
-        if (sm.best_alpha[i] < lo) lo = sm.best_alpha[i];
+        if (SMX.best_alpha[i] < lo) lo = SMX.best_alpha[i];
       for (int i = 0; i < m; ++i) {
-        sm.best_alpha[i] = __dsub_rn(sm.best_alpha[i], lo);
-        sm.alpha_star[i] = sm.best_alpha[i];
+        SMX.best_alpha[i] = __dsub_rn(SMX.best_alpha[i], lo);
+        SMX.alpha_star[i] = SMX.best_alpha[i];
       }
     }
     __syncthreads();
-    double db = eval_dual(sm.best_alpha, true, mo);  // :313
+    double db = eval_dual(SMX.best_alpha, true, mo);  // :313
     bool integral = true;
     for (int i = 0; i < m; ++i)
-      if (fabs(__dsub_rn(sm.c[i], round(sm.c[i]))) > 1e-9) integral = false;
+      if (fabs(__dsub_rn(SMX.c[i], round(SMX.c[i]))) > 1e-9) integral = false;
     if (tid == 0) {
-      sm.dual_bound = db;
+      SMX.dual_bound = db;
       for (int i = 0; i < m; ++i)
-        sm.resid[i] = __ddiv_rn(__dsub_rn((double)sm.counts[i], sm.c[i]), (double)n);
+        SMX.resid[i] = __ddiv_rn(__dsub_rn((double)SMX.counts[i], SMX.c[i]), (double)n);
       if (integral)
-        for (int i = 0; i < m; ++i) sm.target[i] = (int)llround(sm.c[i]);
+        for (int i = 0; i < m; ++i) SMX.target[i] = (int)llround(SMX.c[i]);
     }
     __syncthreads();
     if (integral) {  // :317-321
       double sc = repair();
       if (tid == 0) {
-        sm.score = sc;
-        sm.gap = __dsub_rn(sm.dual_bound, sc);
+        SMX.score = sc;
+        SMX.gap = __dsub_rn(SMX.dual_bound, sc);
       }
     } else if (tid == 0) {
-      sm.score = sm.dual_bound;
-      sm.gap = 0.0;
+      SMX.score = SMX.dual_bound;
+      SMX.gap = 0.0;
     }
     __syncthreads();
   }
 
   // ---- optimize_fractions (routing_opt.cpp:70-136) -------------------------------------
-  // out: sm.fr_w, fr_score, fr_lat, fr_obj, fr_iters, fr_conv, fr_oor
+  // out: SMX.fr_w, fr_score, fr_lat, fr_obj, fr_iters, fr_conv, fr_oor
   __device__ void optimize_fractions(double beta, const rw_opt_context& opt,
                                      const rw_pga_params& p) {
     if (tid == 0) {
       for (int i = 0; i < m; ++i) {
-        sm.w[i] = __ddiv_rn(1.0, (double)m);
-        sm.best_w[i] = sm.w[i];
+        SMX.w[i] = __ddiv_rn(1.0, (double)m);
+        SMX.best_w[i] = SMX.w[i];
       }
-      sm.best_obj = -CUDART_INF;
-      sm.have_warm = 0;
-      sm.fr_iters = 0;
-      sm.fr_conv = 0;
+      SMX.best_obj = -CUDART_INF;
+      SMX.have_warm = 0;
+      SMX.fr_iters = 0;
+      SMX.fr_conv = 0;
     }
     __syncthreads();
     for (int t = 0; t < p.max_iters; ++t) {
       if (tid == 0)
         for (int i = 0; i < m; ++i) {
-          sm.c[i] = __dmul_rn((double)n, sm.w[i]);
-          sm.init[i] = sm.warm[i];
+          SMX.c[i] = __dmul_rn((double)n, SMX.w[i]);
+          SMX.init[i] = SMX.warm[i];
         }
       __syncthreads();
-      solve_dual(p.dual, sm.have_warm != 0);
-      if (sm.status) return;
+      solve_dual(p.dual, SMX.have_warm != 0);
+      if (SMX.status) return;
       if (tid == 0) {
-        for (int i = 0; i < m; ++i) sm.warm[i] = sm.alpha_star[i];
-        sm.have_warm = 1;
-        double lat = system_latency(jb, pidx, m, sm.w, opt.lambda_rps, opt.kappa, nullptr,
+        for (int i = 0; i < m; ++i) SMX.warm[i] = SMX.alpha_star[i];
+        SMX.have_warm = 1;
+        double lat = system_latency(jb, pidx, m, SMX.w, opt.lambda_rps, opt.kappa, nullptr,
                                     nullptr, nullptr);
-        double obj = __dsub_rn(sm.dual_bound, __dmul_rn(beta, __dsub_rn(lat, opt.tau_ms)));
-        if (obj > sm.best_obj) {
-          sm.best_obj = obj;
-          for (int i = 0; i < m; ++i) sm.best_w[i] = sm.w[i];
+        double obj = __dsub_rn(SMX.dual_bound, __dmul_rn(beta, __dsub_rn(lat, opt.tau_ms)));
+        if (obj > SMX.best_obj) {
+          SMX.best_obj = obj;
+          for (int i = 0; i < m; ++i) SMX.best_w[i] = SMX.w[i];
         }
-        sm.fr_iters = t + 1;
-        system_latency_grad(jb, pidx, m, sm.w, opt.lambda_rps, sm.grad);
+        SMX.fr_iters = t + 1;
+        system_latency_grad(jb, pidx, m, SMX.w, opt.lambda_rps, SMX.grad);
         for (int i = 0; i < m; ++i)
-          sm.step[i] = __dadd_rn(
-              sm.w[i], __dmul_rn(p.eta, __dsub_rn(sm.alpha_star[i], __dmul_rn(beta, sm.grad[i]))));
-        if (!project_simplex(m, sm.step, sm.nextw, sm.tmp)) {
-          if (sm.status == 0) sm.status = RW_ERR_VALIDATION;
-          sm.flag = 1;
+          SMX.step[i] = __dadd_rn(
+              SMX.w[i], __dmul_rn(p.eta, __dsub_rn(SMX.alpha_star[i], __dmul_rn(beta, SMX.grad[i]))));
+        if (!project_simplex(m, SMX.step, SMX.nextw, SMX.tmp)) {
+          if (SMX.status == 0) SMX.status = RW_ERR_VALIDATION;
+          SMX.flag = 1;
         } else {
           double moved = 0.0;
-          for (int i = 0; i < m; ++i) moved = smax(moved, fabs(__dsub_rn(sm.nextw[i], sm.w[i])));
-          for (int i = 0; i < m; ++i) sm.w[i] = sm.nextw[i];
-          sm.flag = (moved <= p.w_tol);
-          if (sm.flag) sm.fr_conv = 1;
+          for (int i = 0; i < m; ++i) moved = smax(moved, fabs(__dsub_rn(SMX.nextw[i], SMX.w[i])));
+          for (int i = 0; i < m; ++i) SMX.w[i] = SMX.nextw[i];
+          SMX.flag = (moved <= p.w_tol);
+          if (SMX.flag) SMX.fr_conv = 1;
         }
       }
       __syncthreads();
-      if (sm.status) return;
-      if (sm.flag) break;
+      if (SMX.status) return;
+      if (SMX.flag) break;
     }
     if (tid == 0)
-      for (int i = 0; i < m; ++i) sm.c[i] = __dmul_rn((double)n, sm.best_w[i]);
+      for (int i = 0; i < m; ++i) SMX.c[i] = __dmul_rn((double)n, SMX.best_w[i]);
     __syncthreads();
     solve_dual(p.dual, false);  // canonical cold re-solve (:121-123)
-    if (sm.status) return;
+    if (SMX.status) return;
     if (tid == 0) {
       unsigned oor = 0;
-      double lat = system_latency(jb, pidx, m, sm.best_w, opt.lambda_rps, opt.kappa, &oor,
+      double lat = system_latency(jb, pidx, m, SMX.best_w, opt.lambda_rps, opt.kappa, &oor,
                                   nullptr, nullptr);
-      for (int i = 0; i < m; ++i) sm.fr_w[i] = sm.best_w[i];
-      sm.fr_score = sm.score;
-      sm.fr_lat = lat;
-      sm.fr_obj = __dsub_rn(sm.score, __dmul_rn(beta, __dsub_rn(lat, opt.tau_ms)));
-      sm.fr_oor = oor;
+      for (int i = 0; i < m; ++i) SMX.fr_w[i] = SMX.best_w[i];
+      SMX.fr_score = SMX.score;
+      SMX.fr_lat = lat;
+      SMX.fr_obj = __dsub_rn(SMX.score, __dmul_rn(beta, __dsub_rn(lat, opt.tau_ms)));
+      SMX.fr_oor = oor;
     }
     __syncthreads();
   }
@@ -997,67 +1188,67 @@ struct Solver {
     if (tid == 0) {
       double lo = bp.beta_min, hi = bp.beta_max;
       if (hi < 0.0) {
-        if (!(opt.tau_ms > 0.0)) sm.status = RW_ERR_VALIDATION;
+        if (!(opt.tau_ms > 0.0)) SMX.status = RW_ERR_VALIDATION;
         hi = __ddiv_rn(10.0, opt.tau_ms);
       }
       double eps = bp.epsilon;
       if (eps < 0.0) eps = __ddiv_rn(__dsub_rn(hi, lo), 1024.0);
-      if (!(lo >= 0.0) || !(lo < hi)) sm.status = RW_ERR_VALIDATION;
-      if (!(eps > 0.0)) sm.status = RW_ERR_VALIDATION;
-      sm.lo = lo;
-      sm.hi = hi;
-      sm.eps = eps;
-      sm.b_feasible = 0;
-      sm.b_has = 0;
-      sm.n_trace = 0;
-      sm.beta_star = 0.0;
-      sm.bst_score = sm.bst_lat = sm.bst_obj = 0.0;
-      sm.bst_iters = sm.bst_conv = 0;
-      sm.bst_oor = 0;
+      if (!(lo >= 0.0) || !(lo < hi)) SMX.status = RW_ERR_VALIDATION;
+      if (!(eps > 0.0)) SMX.status = RW_ERR_VALIDATION;
+      SMX.lo = lo;
+      SMX.hi = hi;
+      SMX.eps = eps;
+      SMX.b_feasible = 0;
+      SMX.b_has = 0;
+      SMX.n_trace = 0;
+      SMX.beta_star = 0.0;
+      SMX.bst_score = SMX.bst_lat = SMX.bst_obj = 0.0;
+      SMX.bst_iters = SMX.bst_conv = 0;
+      SMX.bst_oor = 0;
       for (int i = 0; i < m; ++i) {
-        sm.w_star[i] = 0.0;
-        sm.bst_w[i] = 0.0;
+        SMX.w_star[i] = 0.0;
+        SMX.bst_w[i] = 0.0;
       }
-      sm.tr_best_lat = 0.0;
-      sm.tr_best_score = 0.0;
+      SMX.tr_best_lat = 0.0;
+      SMX.tr_best_score = 0.0;
     }
     __syncthreads();
-    if (sm.status) return;
-    while (__dsub_rn(sm.hi, sm.lo) > sm.eps) {
-      const double mid = __dmul_rn(0.5, __dadd_rn(sm.lo, sm.hi));
+    if (SMX.status) return;
+    while (__dsub_rn(SMX.hi, SMX.lo) > SMX.eps) {
+      const double mid = __dmul_rn(0.5, __dadd_rn(SMX.lo, SMX.hi));
       optimize_fractions(mid, opt, bp.pga);
-      if (sm.status) return;
+      if (SMX.status) return;
       if (tid == 0) {
-        bool ok = sm.fr_lat <= opt.tau_ms && sm.fr_oor == 0u;
-        if (trace && sm.n_trace < trace_cap) {
-          trace[sm.n_trace].beta = mid;
-          trace[sm.n_trace].score = sm.fr_score;
-          trace[sm.n_trace].latency_ms = sm.fr_lat;
-          trace[sm.n_trace].feasible = ok ? 1 : 0;
-          trace[sm.n_trace].pad_ = 0;
+        bool ok = SMX.fr_lat <= opt.tau_ms && SMX.fr_oor == 0u;
+        if (trace && SMX.n_trace < trace_cap) {
+          trace[SMX.n_trace].beta = mid;
+          trace[SMX.n_trace].score = SMX.fr_score;
+          trace[SMX.n_trace].latency_ms = SMX.fr_lat;
+          trace[SMX.n_trace].feasible = ok ? 1 : 0;
+          trace[SMX.n_trace].pad_ = 0;
         }
-        if (sm.n_trace == 0 || sm.fr_lat < sm.tr_best_lat) {  // setup_search.cpp:200-202
-          sm.tr_best_lat = sm.fr_lat;
-          sm.tr_best_score = sm.fr_score;
+        if (SMX.n_trace == 0 || SMX.fr_lat < SMX.tr_best_lat) {  // setup_search.cpp:200-202
+          SMX.tr_best_lat = SMX.fr_lat;
+          SMX.tr_best_score = SMX.fr_score;
         }
-        sm.n_trace++;
+        SMX.n_trace++;
         if (ok) {
-          sm.b_feasible = 1;
-          sm.b_has = 1;
-          sm.beta_star = mid;
+          SMX.b_feasible = 1;
+          SMX.b_has = 1;
+          SMX.beta_star = mid;
           for (int i = 0; i < m; ++i) {
-            sm.w_star[i] = sm.fr_w[i];
-            sm.bst_w[i] = sm.fr_w[i];
+            SMX.w_star[i] = SMX.fr_w[i];
+            SMX.bst_w[i] = SMX.fr_w[i];
           }
-          sm.bst_score = sm.fr_score;
-          sm.bst_lat = sm.fr_lat;
-          sm.bst_obj = sm.fr_obj;
-          sm.bst_iters = sm.fr_iters;
-          sm.bst_conv = sm.fr_conv;
-          sm.bst_oor = sm.fr_oor;
-          sm.hi = mid;
+          SMX.bst_score = SMX.fr_score;
+          SMX.bst_lat = SMX.fr_lat;
+          SMX.bst_obj = SMX.fr_obj;
+          SMX.bst_iters = SMX.fr_iters;
+          SMX.bst_conv = SMX.fr_conv;
+          SMX.bst_oor = SMX.fr_oor;
+          SMX.hi = mid;
         } else {
-          sm.lo = mid;
+          SMX.lo = mid;
         }
       }
       __syncthreads();
@@ -1066,11 +1257,13 @@ struct Solver {
 
   __device__ void reset_counters() {
     if (tid == 0) {
-      sm.status = 0;
-      sm.eval_passes = 0;
-      sm.polish_passes = 0;
-      sm.repair_calls = 0;
-      for (int i = 0; i < MM; ++i) sm.zero[i] = 0.0;
+      SMX.status = 0;
+      SMX.eval_passes = 0;
+      SMX.polish_passes = 0;
+      SMX.repair_calls = 0;
+      SMX.pol_delta = 1e-3;
+      for (int i = 0; i < 8; ++i) SMX.prof[i] = 0;
+      for (int i = 0; i < MM; ++i) SMX.zero[i] = 0.0;
     }
     __syncthreads();
   }
@@ -1080,39 +1273,41 @@ struct Solver {
     pidx = jb.prof_idx + (size_t)k * m;
     reset_counters();
     optimize_beta(jb.opt, jb.bp, nullptr, 0);
-    int bisect = sm.n_trace;
+    int bisect = SMX.n_trace;
     double e_score = 0.0, e_lat = 0.0;
-    if (!sm.status && !sm.b_feasible) {
-      if (sm.n_trace > 0) {
-        e_score = sm.tr_best_score;
-        e_lat = sm.tr_best_lat;
+    if (!SMX.status && !SMX.b_feasible) {
+      if (SMX.n_trace > 0) {
+        e_score = SMX.tr_best_score;
+        e_lat = SMX.tr_best_lat;
       } else {  // degenerate bracket: evaluate the top penalty once
         double beta_hi = jb.bp.beta_max;
         if (beta_hi < 0.0) beta_hi = __ddiv_rn(10.0, jb.opt.tau_ms);
         optimize_fractions(beta_hi, jb.opt, jb.bp.pga);
-        e_score = sm.fr_score;
-        e_lat = sm.fr_lat;
+        e_score = SMX.fr_score;
+        e_lat = SMX.fr_lat;
       }
     }
     __syncthreads();
     if (tid == 0) {
       rec->setup_id = jb.setup_ids ? jb.setup_ids[k] : k;
-      rec->status = sm.status;
-      rec->feasible = (!sm.status && sm.b_feasible) ? 1 : 0;
-      rec->score = sm.b_feasible ? sm.bst_score : e_score;
-      rec->latency_ms = sm.b_feasible ? sm.bst_lat : e_lat;
-      rec->beta = sm.b_feasible ? sm.beta_star : 0.0;
+      rec->status = SMX.status;
+      rec->feasible = (!SMX.status && SMX.b_feasible) ? 1 : 0;
+      rec->score = SMX.b_feasible ? SMX.bst_score : e_score;
+      rec->latency_ms = SMX.b_feasible ? SMX.bst_lat : e_lat;
+      rec->beta = SMX.b_feasible ? SMX.beta_star : 0.0;
       for (int i = 0; i < RW_MAX_MODELS; ++i)
-        rec->w[i] = (sm.b_feasible && i < m) ? sm.bst_w[i] : 0.0;
-      rec->out_of_range = sm.b_feasible ? sm.bst_oor : 0u;
+        rec->w[i] = (SMX.b_feasible && i < m) ? SMX.bst_w[i] : 0.0;
+      rec->out_of_range = SMX.b_feasible ? SMX.bst_oor : 0u;
       rec->bisect_steps = bisect;
-      rec->eval_passes = sm.eval_passes;
-      rec->polish_passes = sm.polish_passes;
-      rec->repair_calls = sm.repair_calls;
+      rec->eval_passes = SMX.eval_passes;
+      rec->polish_passes = SMX.polish_passes;
+      rec->repair_calls = SMX.repair_calls;
     }
     __syncthreads();
   }
 };
+
+#undef SMX
 
 // ---------------------------------------------------------------------------------------
 template <int MM, int L, int T>
@@ -1123,7 +1318,7 @@ __global__ void __launch_bounds__(T) solver_kernel(const Job jb) {
   const int slot = blockIdx.x;
   uint8_t* mo = jb.ws_model_of + (size_t)slot * jb.n;
   unsigned long long* keys = reinterpret_cast<unsigned long long*>(jb.ws_keys) + (size_t)slot * jb.n;
-  Solver<MM, L, T> s(sm, jb, mo, keys);
+  Solver<MM, L, T> s(jb, mo, keys);
   const int tid = threadIdx.x;
   const int m = jb.m, n = jb.n;
 
@@ -1136,6 +1331,9 @@ __global__ void __launch_bounds__(T) solver_kernel(const Job jb) {
       const long long k = (long long)jb.shard_rank + item * jb.shard_count;
       if (k >= jb.n_items) break;
       s.evaluate_setup(k, jb.records + item);
+      if (tid == 0 && jb.prof_out)
+        for (int i = 0; i < 8; ++i)
+          atomicAdd((unsigned long long*)jb.prof_out + i, (unsigned long long)sm.prof[i]);
       if (tid == 0 && sm.status && jb.status_out) atomicCAS(jb.status_out, 0, sm.status);
     }
     return;
@@ -1218,6 +1416,20 @@ __global__ void __launch_bounds__(T) solver_kernel(const Job jb) {
       o->pad_ = 0;
       o->eval_passes = sm.eval_passes;
     }
+  } else if (jb.kind == JOB_BENCH_PASS) {
+    // diagnostics: trip_count eval passes at fixed prices (alpha, c from the job)
+    if (tid == 0)
+      for (int i = 0; i < m; ++i) {
+        sm.c[i] = jb.c[i];
+        sm.alpha[i] = jb.vec[i];
+      }
+    __syncthreads();
+    double g = 0.0;
+    for (int it = 0; it < jb.trace_cap; ++it) g = s.eval_dual(sm.alpha, true, nullptr);
+    if (tid == 0) {
+      jb.dvec_out[0] = g;
+      for (int i = 0; i < m; ++i) jb.ivec_out[i] = sm.counts[i];
+    }
   } else if (jb.kind == JOB_SIMPLEX) {
     if (tid == 0) {
       if (!project_simplex(m, jb.vec, jb.dvec_out, sm.tmp)) sm.status = RW_ERR_VALIDATION;
@@ -1234,6 +1446,8 @@ __global__ void __launch_bounds__(T) solver_kernel(const Job jb) {
   }
   __syncthreads();
   if (tid == 0 && sm.status && jb.status_out) atomicCAS(jb.status_out, 0, sm.status);
+  if (tid == 0 && jb.prof_out)
+    for (int i = 0; i < 8; ++i) atomicAdd((unsigned long long*)jb.prof_out + i, (unsigned long long)sm.prof[i]);
 }
 
 }  // namespace rw

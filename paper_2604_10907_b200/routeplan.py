@@ -471,6 +471,14 @@ class Engine:
         self._profiles_key = None
         return self
 
+    def set_profiling(self, enable: bool = True):
+        self._chk(self.L.rw_set_profiling(self.h, 1 if enable else 0))
+
+    def profile(self) -> np.ndarray:
+        out = np.zeros(8, np.int64)
+        self._chk(self.L.rw_get_profile(self.h, lptr(out)))
+        return out
+
     def last_kernel_ms(self) -> float:
         ms = C.c_double()
         self._chk(self.L.rw_last_kernel_ms(self.h, C.byref(ms)))
