@@ -134,6 +134,7 @@ typedef struct {
   double score;
   double latency_ms;
   double beta;
+  double tau_ms; /* the SLO this record was solved for */
   double w[RW_MAX_MODELS];
   uint32_t out_of_range;
   int32_t bisect_steps;
@@ -208,10 +209,22 @@ int rw_sweep(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
              const int32_t* profile_index, const rw_opt_context* opt,
              const rw_beta_params* params, int32_t shard_rank, int32_t shard_count,
              rw_setup_record* out_records, int64_t* n_out);
-/* Same, asynchronous: records stay in device memory (ctx-owned) until rw_sweep_fetch. */
+/* SLO sweep: every (setup, tau) pair of n_setups x n_slo is one independent instance
+ * (the reference takes one tau per select_setup call; this batches them in one launch).
+ * Instance k = slo * n_setups + setup; sharding is over k.  opt->tau_ms is ignored;
+ * params[t] are SLO t's search parameters (n_slo entries). */
+int rw_sweep_slo(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                 const int32_t* profile_index, int32_t n_slo, const double* tau_ms,
+                 const rw_opt_context* opt, const rw_beta_params* params, int32_t shard_rank,
+                 int32_t shard_count, rw_setup_record* out_records, int64_t* n_out);
+/* Asynchronous variants: records stay in device memory (ctx-owned) until rw_sweep_fetch. */
 int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                    const int32_t* profile_index, const rw_opt_context* opt,
                    const rw_beta_params* params, int32_t shard_rank, int32_t shard_count);
+int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                       const int32_t* profile_index, int32_t n_slo, const double* tau_ms,
+                       const rw_opt_context* opt, const rw_beta_params* params,
+                       int32_t shard_rank, int32_t shard_count);
 int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out_records, int64_t* n_out);
 
 /* Order-deterministic winner (setup_search.cpp:246-253): feasible, max score, then min

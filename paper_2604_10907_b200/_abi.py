@@ -71,7 +71,8 @@ class rw_beta_result(C.Structure):
 class rw_setup_record(C.Structure):
     _fields_ = [("setup_id", C.c_int64), ("feasible", C.c_int32), ("status", C.c_int32),
                 ("score", C.c_double), ("latency_ms", C.c_double), ("beta", C.c_double),
-                ("w", C.c_double * RW_MAX_MODELS), ("out_of_range", C.c_uint32),
+                ("tau_ms", C.c_double), ("w", C.c_double * RW_MAX_MODELS),
+                ("out_of_range", C.c_uint32),
                 ("bisect_steps", C.c_int32), ("eval_passes", C.c_int64),
                 ("polish_passes", C.c_int64), ("repair_calls", C.c_int64)]
 
@@ -79,7 +80,7 @@ class rw_setup_record(C.Structure):
 # numpy view of rw_setup_record (same layout) for zero-copy record arrays
 RECORD_DTYPE = np.dtype([("setup_id", "<i8"), ("feasible", "<i4"), ("status", "<i4"),
                          ("score", "<f8"), ("latency_ms", "<f8"), ("beta", "<f8"),
-                         ("w", "<f8", (RW_MAX_MODELS,)), ("out_of_range", "<u4"),
+                         ("tau_ms", "<f8"), ("w", "<f8", (RW_MAX_MODELS,)), ("out_of_range", "<u4"),
                          ("bisect_steps", "<i4"), ("eval_passes", "<i8"),
                          ("polish_passes", "<i8"), ("repair_calls", "<i8")])
 assert RECORD_DTYPE.itemsize == C.sizeof(rw_setup_record)
@@ -128,6 +129,12 @@ def lib():
         L.rw_sweep_async.argtypes = [C.c_void_p, C.c_int64, _lp, _ip,
                                      C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
                                      C.c_int32, C.c_int32]
+        L.rw_sweep_slo.argtypes = [C.c_void_p, C.c_int64, _lp, _ip, C.c_int32, _dp,
+                                   C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
+                                   C.c_int32, C.c_int32, C.c_void_p, _lp]
+        L.rw_sweep_slo_async.argtypes = [C.c_void_p, C.c_int64, _lp, _ip, C.c_int32, _dp,
+                                         C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
+                                         C.c_int32, C.c_int32]
         L.rw_sweep_fetch.argtypes = [C.c_void_p, C.c_void_p, _lp]
         L.rw_reduce_records.argtypes = [C.c_int64, C.c_void_p]
         L.rw_synth_scores.argtypes = [C.c_int32, C.c_int32, _dp, _dp, C.c_uint64, _dp]

@@ -618,23 +618,29 @@ int rw_optimize_beta(rw_ctx* ctx, const int32_t* pidx, const rw_opt_context* opt
   return RW_OK;
 }
 
-int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
-                   const int32_t* pidx, const rw_opt_context* opt, const rw_beta_params* params,
-                   int32_t shard_rank, int32_t shard_count) {
+int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                       const int32_t* pidx, int32_t n_slo, const double* taus,
+                       const rw_opt_context* opt, const rw_beta_params* params,
+                       int32_t shard_rank, int32_t shard_count) {
   int rc;
   if ((rc = need_inputs(ctx, true))) return rc;
-  if (!opt || !params) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: null argument");
+  if (!opt || !params || !taus) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: null argument");
   if (shard_count < 1 || shard_rank < 0 || shard_rank >= shard_count)
     return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: bad shard");
-  if (n_setups < 0) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: negative setup count");
+  if (n_setups < 0 || n_slo < 1)
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: bad setup / SLO count");
   if (!(opt->lambda_rps > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "arrival rate must be positive");
   if (!(opt->kappa > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "kappa must be positive");
   if (n_setups > 0) {
-    if ((rc = check_beta_params(ctx, opt, params))) return rc;
+    for (int32_t t = 0; t < n_slo; ++t) {
+      rw_opt_context o = *opt;
+      o.tau_ms = taus[t];
+      if ((rc = check_beta_params(ctx, &o, params + t))) return rc;
+    }
     if ((rc = validate_profile_index(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
   }
-  const int64_t items =
-      n_setups > shard_rank ? (n_setups - shard_rank + shard_count - 1) / shard_count : 0;
+  const int64_t inst = n_setups * (int64_t)n_slo;
+  const int64_t items = inst > shard_rank ? (inst - shard_rank + shard_count - 1) / shard_count : 0;
   ctx->pending_records = items;
   if (items == 0) return RW_OK;
   CK(cudaSetDevice(ctx->device));
@@ -642,7 +648,10 @@ int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
   {
     void* p = ctx->d_setup_ids;
     size_t cap = ctx->setup_ids_cap;
-    if ((rc = ensure(ctx, &p, &cap, sizeof(int64_t) * n_setups))) return rc;
+    if ((rc = ensure(ctx, &p, &cap,
+                     sizeof(int64_t) * n_setups + (sizeof(double) + sizeof(rw_beta_params)) * n_slo +
+                         64)))
+      return rc;
     ctx->d_setup_ids = static_cast<int64_t*>(p);
     ctx->setup_ids_cap = cap;
     std::vector<int64_t> ids;
@@ -653,6 +662,10 @@ int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
     }
     CK(cudaMemcpyAsync(ctx->d_setup_ids, setup_ids, sizeof(int64_t) * n_setups,
                        cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups, taus, sizeof(double) * n_slo,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups + n_slo, params,
+                       sizeof(rw_beta_params) * n_slo, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // `ids` is stack-owned
   }
   {
@@ -667,13 +680,28 @@ int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
   rw::Job j = base_job(ctx, rw::JOB_SWEEP);
   j.prof_idx = ctx->d_prof_idx;
   j.setup_ids = ctx->d_setup_ids;
-  j.n_items = n_setups;
+  j.n_items = inst;
+  j.n_setups = n_setups;
+  j.taus = reinterpret_cast<const double*>(ctx->d_setup_ids + n_setups);
+  j.bps = reinterpret_cast<const rw_beta_params*>(ctx->d_setup_ids + n_setups + n_slo);
   j.shard_rank = shard_rank;
   j.shard_count = shard_count;
   j.opt = *opt;
   j.bp = *params;
   j.records = ctx->d_records;
   return run(ctx, j, grid);
+}
+
+int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                   const int32_t* pidx, const rw_opt_context* opt, const rw_beta_params* params,
+                   int32_t shard_rank, int32_t shard_count) {
+  if (!opt) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: null argument");
+  if (n_setups > 0 && params) {
+    int rc = check_beta_params(ctx, opt, params);
+    if (rc) return rc;
+  }
+  return rw_sweep_slo_async(ctx, n_setups, setup_ids, pidx, 1, &opt->tau_ms, opt, params,
+                            shard_rank, shard_count);
 }
 
 int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out, int64_t* n_out) {
@@ -696,6 +724,16 @@ int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out, int64_t* n_out) {
   if (out)
     CK(cudaMemcpy(out, ctx->d_records, sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost));
   return RW_OK;
+}
+
+int rw_sweep_slo(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const int32_t* pidx,
+                 int32_t n_slo, const double* taus, const rw_opt_context* opt,
+                 const rw_beta_params* params, int32_t shard_rank, int32_t shard_count,
+                 rw_setup_record* out, int64_t* n_out) {
+  int rc = rw_sweep_slo_async(ctx, n_setups, setup_ids, pidx, n_slo, taus, opt, params,
+                              shard_rank, shard_count);
+  if (rc) return rc;
+  return rw_sweep_fetch(ctx, out, n_out);
 }
 
 int rw_sweep(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const int32_t* pidx,

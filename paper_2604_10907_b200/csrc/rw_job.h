@@ -29,7 +29,10 @@ struct Job {
   // setups
   const int32_t* prof_idx;  // [n_items * m]
   const int64_t* setup_ids;
-  int64_t n_items;
+  int64_t n_items;      // instances = n_setups * n_slo
+  int64_t n_setups;
+  const double* taus;   // [n_slo] (JOB_SWEEP); null -> opt.tau_ms
+  const rw_beta_params* bps;  // [n_slo] per-SLO params (JOB_SWEEP); null -> bp
   int32_t shard_rank, shard_count;
   rw_opt_context opt;
   rw_beta_params bp;

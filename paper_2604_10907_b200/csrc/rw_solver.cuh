@@ -72,8 +72,8 @@ template <int MM, int L, int T>
 struct Smem {
   static constexpr int R = L * T;       // rows per tile
   static constexpr int W = T / 32;      // warps
-  static constexpr int BPAD = T * (L | 1);
-  double b[BPAD];                       // tile's b_j, chunk t at [t*(L|1), +L) (odd stride)
+  static constexpr int BPAD = L * T + (L * T) / 8 + 1;
+  double b[BPAD];                       // tile's b_j at k + k/8 (conflict-free both ways)
   long long q0[T], q1[T];               // pieces: SAFE -> (Q0, Q1); RAW -> (start, count)
   double scan_x[W], scan_y[W];
   unsigned hist[256];
@@ -264,8 +264,9 @@ struct Solver {
   //    A segmented warp scan composes runs of SAFE chunks of one binade into a single
   //    piece, so each warp publishes ~1 piece (a few around binade crossings).
   //  phase 3 (thread 0): apply the pieces in order to the exact running sum S.
-  static constexpr int LP = L | 1;  // odd chunk stride in smem: conflict-free chunk reads
-  __device__ __forceinline__ static int bpos(int k) { return (k / L) * LP + (k % L); }
+  // b_j of tile row k lives at k + k/8: coalesced writes in phase 1 and, for L = 24, the
+  // chunk reads of phase 2 (lane t at 27t + r) are bank-conflict free.
+  __device__ __forceinline__ static int bpos(int k) { return k + (k >> 3); }
 
   // quanta of one |b| for u = 2^(base_sh - 1023 - 52): floor and half-way flag (exact, INT)
   __device__ __forceinline__ static long long quanta_floor(double ab, int base_sh, bool& tie,
@@ -290,10 +291,15 @@ struct Solver {
   __device__ void pass(int mode, const double* alpha_s, bool want_counts, uint8_t* mo_out,
                        const uint8_t* mo_in) {
     if (mode == PASS_EVAL) {
-      if (m == MM) pass_t<PASS_EVAL, true>(n, alpha_s, want_counts, mo_out, mo_in);
-      else pass_t<PASS_EVAL, false>(n, alpha_s, want_counts, mo_out, mo_in);
+      if (m == MM) {
+        if (mo_out) pass_t<PASS_EVAL, true, true>(n, alpha_s, want_counts, mo_out, mo_in);
+        else pass_t<PASS_EVAL, true, false>(n, alpha_s, want_counts, mo_out, mo_in);
+      } else {
+        if (mo_out) pass_t<PASS_EVAL, false, true>(n, alpha_s, want_counts, mo_out, mo_in);
+        else pass_t<PASS_EVAL, false, false>(n, alpha_s, want_counts, mo_out, mo_in);
+      }
     } else {
-      pass_t<PASS_FIXED, false>(n, alpha_s, want_counts, mo_out, mo_in);
+      pass_t<PASS_FIXED, false, false>(n, alpha_s, want_counts, mo_out, mo_in);
     }
   }
 
@@ -301,7 +307,7 @@ struct Solver {
   static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : 2);
   static_assert(L % G == 0, "L must be a multiple of the load group");
 
-  template <int MODE, bool FULLM>
+  template <int MODE, bool FULLM, bool WMO>
   __device__ __noinline__ void pass_t(const int n_, const double* alpha_s, const bool want_counts,
                                       uint8_t* mo_out, const uint8_t* mo_in) {
     const int tid_ = threadIdx.x, lane_ = tid_ & 31, wid_ = tid_ >> 5;
@@ -391,7 +397,7 @@ struct Solver {
                   pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
               }
             }
-            if (mo_out) mo_out[base + k] = (uint8_t)arg;
+            if (WMO) mo_out[base + k] = (uint8_t)arg;
           }
         }
       }
@@ -415,31 +421,33 @@ struct Solver {
       long long t_p2 = clock64();
       if (tid_ == 0) SMX.prof[0] += t_p2 - t_p1;
       // -- phase 2 ----------------------------------------------------------------------
+      static_assert(L % 8 == 0, "chunk addressing assumes L % 8 == 0");
       const int c0 = tid_ * L;
       const int cnt = max(0, min(L, len - c0));
-      const double* bch = SMX.b + tid_ * LP;
+      const double* bch = SMX.b + bpos(c0);
+      double bl[L];
       double ps = 0.0;
       unsigned orhi = 0u, andhi = 0xffffffffu;
 #pragma unroll
       for (int r = 0; r < L; ++r) {
+        bl[r] = 0.0;
         if (r < cnt) {
-          const double x = bch[r];
-          ps += x;
-          const unsigned hi = (unsigned)__double2hiint(x);
+          bl[r] = bch[r + (r >> 3)];
+          ps += bl[r];
+          const unsigned hi = (unsigned)__double2hiint(bl[r]);
           orhi |= hi;
           andhi &= hi;
         }
       }
-      const bool allpos = (orhi >> 31) == 0u;    // every b has its sign bit clear (incl. +0)
-      const bool allneg = (andhi >> 31) != 0u;   // every b has its sign bit set
+      const bool allpos = (orhi >> 31) == 0u;   // every b has its sign bit clear (incl. +0)
+      const bool allneg = (andhi >> 31) != 0u;  // every b has its sign bit set
       double pa;
       if (allpos) pa = ps;
       else if (allneg) pa = -ps;
       else {
         pa = 0.0;
 #pragma unroll
-        for (int r = 0; r < L; ++r)
-          if (r < cnt) pa += fabs(bch[r]);
+        for (int r = 0; r < L; ++r) pa += fabs(bl[r]);
       }
       // block exclusive scan of (ps, pa) — approximate; used only behind a margin
       double ix = ps, iy = pa;
@@ -501,45 +509,54 @@ struct Solver {
         } else {
           double P = P0, A = A0;
           bool ok = true;
-          for (int r = 0; r <= cnt && ok; ++r) {
-            const double x = (r < cnt) ? bch[r] : 0.0;
-            const double E = (double)(jg + r + 64) * 0x1p-51 * (A + fabs(x));
-            int e, ng;
-            if (!in_binade(P, E, e, ng)) ok = false;
-            else if (r == 0) {
-              e_ref = e;
-              neg_ref = ng;
-            } else if (e != e_ref || ng != neg_ref) ok = false;
-            P += x;
-            A += fabs(x);
+#pragma unroll
+          for (int r = 0; r <= L; ++r) {
+            if (r <= cnt && ok) {
+              const double x = (r < cnt) ? bl[r] : 0.0;
+              const double E = (double)(jg + r + 64) * 0x1p-51 * (A + fabs(x));
+              int e, ng;
+              if (!in_binade(P, E, e, ng)) ok = false;
+              else if (r == 0) {
+                e_ref = e;
+                neg_ref = ng;
+              } else if (e != e_ref || ng != neg_ref) ok = false;
+              P += x;
+              A += fabs(x);
+            }
           }
           if (ok) kind = PIECE_SAFE;
         }
       }
       long long Q0 = 0, Q1 = 0;
       if (kind == PIECE_SAFE) {
-        // q_j = round(b_j / u) with u = 2^(e-52): exact integer quanta of each b_j
-        const int base_sh = 1023 + e_ref;
+        // q_j = round(b_j / u), u = 2^(e-52).  Monotone fast path in FP64: y = |b| * 2^(52-e)
+        // is exact and < 2^52 (S and S + b share the binade), so t = y + 2^52 rounds y to
+        // the integer grid (RNE) and bits(t) - bits(2^52) is that integer; a half-way
+        // y (|t - 2^52 - y| == 1/2) is a tie whose rounding depends on S — slow path.
         bool tie_any = false;
-        if (allpos) {
+        if (allpos || allneg) {
+          const double scale = __longlong_as_double((long long)(52 - e_ref + 1023) << 52);
+          unsigned long long acc = 0ull;
 #pragma unroll
           for (int r = 0; r < L; ++r) {
             if (r < cnt) {
-              bool tie, above;
-              long long q = quanta_floor(bch[r], base_sh, tie, above);
-              Q0 += q + (above ? 1 : 0);
-              tie_any |= tie;
+              const double y = fabs(bl[r]) * scale;
+              const double t = y + 0x1p52;
+              acc += (unsigned long long)__double_as_longlong(t) - 0x4330000000000000ull;
+              tie_any |= (fabs((t - 0x1p52) - y) == 0.5);
             }
           }
+          Q0 = allpos ? (long long)acc : -(long long)acc;
           Q1 = Q0;
         }
-        if (!allpos || tie_any) {  // general: signed b, two parity tracks for ties
+        if (!(allpos || allneg) || tie_any) {  // general: signed b, two parity tracks
+          const int base_sh = 1023 + e_ref;
           Q0 = 0;
           Q1 = 0;
           for (int r = 0; r < cnt; ++r) {
-            const double x = bch[r];
+            const double x = bch[r + (r >> 3)];
             bool tie, above;
-            long long q = quanta_floor(x, base_sh, tie, above);
+            const long long q = quanta_floor(x, base_sh, tie, above);
             const bool negb = x < 0.0;
             if (tie) {  // |x|/u = q + 1/2; RNE picks the neighbour leaving S/u even
               const long long lo = negb ? -q - 1 : q;
@@ -578,7 +595,7 @@ struct Solver {
       if (tail) {
         const int slot = wid_ * 32 + __popc(tmask & ((1u << lane_) - 1u));
         SMX.pkind[slot] = (unsigned char)kind;
-        SMX.q0[slot] = (kind == PIECE_SAFE) ? Q0 : (long long)(tid_ * LP);
+        SMX.q0[slot] = (kind == PIECE_SAFE) ? Q0 : (long long)c0;
         SMX.q1[slot] = (kind == PIECE_SAFE) ? Q1 : (long long)cnt;
       }
       if (lane_ == 0) SMX.wcnt[wid_] = __popc(tmask);
@@ -596,9 +613,8 @@ struct Solver {
             if (SMX.pkind[slot] == PIECE_SAFE) {
               S = apply_quanta(S, x0, x1);
             } else {
-              const double* rb = SMX.b + (int)x0;
-              const int rc = (int)x1;
-              for (int r = 0; r < rc; ++r) S = __dadd_rn(S, rb[r]);
+              const int k0 = (int)x0, rc = (int)x1;
+              for (int r = 0; r < rc; ++r) S = __dadd_rn(S, SMX.b[bpos(k0 + r)]);
             }
           }
         }
@@ -1269,10 +1285,14 @@ struct Solver {
   }
 
   // ---- select_setup's evaluate (setup_search.cpp:187-211) -> one record ---------------
-  __device__ void evaluate_setup(long long k, rw_setup_record* rec) {
+  __device__ void evaluate_setup(long long inst, rw_setup_record* rec) {
+    const long long k = inst % jb.n_setups;
+    rw_opt_context opt = jb.opt;
+    if (jb.taus) opt.tau_ms = jb.taus[inst / jb.n_setups];
+    const rw_beta_params bp = jb.bps ? jb.bps[inst / jb.n_setups] : jb.bp;
     pidx = jb.prof_idx + (size_t)k * m;
     reset_counters();
-    optimize_beta(jb.opt, jb.bp, nullptr, 0);
+    optimize_beta(opt, bp, nullptr, 0);
     int bisect = SMX.n_trace;
     double e_score = 0.0, e_lat = 0.0;
     if (!SMX.status && !SMX.b_feasible) {
@@ -1280,9 +1300,9 @@ struct Solver {
         e_score = SMX.tr_best_score;
         e_lat = SMX.tr_best_lat;
       } else {  // degenerate bracket: evaluate the top penalty once
-        double beta_hi = jb.bp.beta_max;
-        if (beta_hi < 0.0) beta_hi = __ddiv_rn(10.0, jb.opt.tau_ms);
-        optimize_fractions(beta_hi, jb.opt, jb.bp.pga);
+        double beta_hi = bp.beta_max;
+        if (beta_hi < 0.0) beta_hi = __ddiv_rn(10.0, opt.tau_ms);
+        optimize_fractions(beta_hi, opt, bp.pga);
         e_score = SMX.fr_score;
         e_lat = SMX.fr_lat;
       }
@@ -1295,6 +1315,7 @@ struct Solver {
       rec->score = SMX.b_feasible ? SMX.bst_score : e_score;
       rec->latency_ms = SMX.b_feasible ? SMX.bst_lat : e_lat;
       rec->beta = SMX.b_feasible ? SMX.beta_star : 0.0;
+      rec->tau_ms = opt.tau_ms;
       for (int i = 0; i < RW_MAX_MODELS; ++i)
         rec->w[i] = (SMX.b_feasible && i < m) ? SMX.bst_w[i] : 0.0;
       rec->out_of_range = SMX.b_feasible ? SMX.bst_oor : 0u;
@@ -1311,7 +1332,7 @@ struct Solver {
 
 // ---------------------------------------------------------------------------------------
 template <int MM, int L, int T>
-__global__ void __launch_bounds__(T) solver_kernel(const Job jb) {
+__global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kernel(const Job jb) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = Smem<MM, L, T>;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);

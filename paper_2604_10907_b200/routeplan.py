@@ -584,18 +584,28 @@ class Engine:
                                   C.byref(n_out)))
         return recs[: n_out.value]
 
-    def sweep_async(self, profile_index, setup_ids, opt, params, shard_rank=0, shard_count=1):
+    def sweep_slo(self, profile_index, setup_ids, taus, opt: OptimizeContext,
+                  params: BetaSearchParams = BetaSearchParams(), shard_rank=0, shard_count=1):
+        """All (setup, tau) instances in one launch -> records (tau-major instance order)."""
+        self.sweep_async(profile_index, setup_ids, opt, params, shard_rank, shard_count, taus)
+        return self.sweep_fetch()
+
+    def sweep_async(self, profile_index, setup_ids, opt, params, shard_rank=0, shard_count=1,
+                    taus=None):
         pi = np.ascontiguousarray(profile_index, np.int32).reshape(-1)
         S = len(pi) // max(self.m, 1)
         ids = np.ascontiguousarray(setup_ids if setup_ids is not None else np.arange(S),
                                    np.int64)
-        self._pending = (pi, ids, S, shard_rank, shard_count)
-        oc, bp = opt.c(), params.c()
-        self._chk(self.L.rw_sweep_async(self.h, S, lptr(ids), iptr(pi), C.byref(oc),
-                                        C.byref(bp), shard_rank, shard_count))
+        t = np.ascontiguousarray([opt.tau_ms] if taus is None else taus, np.float64)
+        plist = params if isinstance(params, (list, tuple)) else [params] * len(t)
+        bps = (_abi.rw_beta_params * len(t))(*[q.c() for q in plist])
+        self._pending = (pi, ids, t, S * len(t), shard_rank, shard_count)
+        oc = opt.c()
+        self._chk(self.L.rw_sweep_slo_async(self.h, S, lptr(ids), iptr(pi), len(t), dptr(t),
+                                            C.byref(oc), bps, shard_rank, shard_count))
 
     def sweep_fetch(self):
-        _, _, S, r, cnt = self._pending
+        _, _, _, S, r, cnt = self._pending
         cap = max(1, (S - r + cnt - 1) // cnt)
         recs = np.zeros(cap, dtype=_abi.RECORD_DTYPE)
         n_out = C.c_int64()

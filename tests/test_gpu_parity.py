@@ -181,3 +181,34 @@ def test_sweep_c1_truncated_vs_oracle(eng, oracle):
         assert bits(r["latency_ms"]) == bits(ref["latency_ms"])
         assert bits(r["beta"]) == bits(ref["beta"])
         assert int(r["eval_passes"]) == ref["eval_passes"]
+
+
+def test_sweep_slo_batch_matches_single_slo(eng, oracle):
+    """(setup, tau) batching: records equal per-SLO sweeps and the C oracle."""
+    from oracle import Params, ProfileTable
+    cfg = wl.config("C2", n=3000)
+    inp = wl.build_inputs(cfg, limit=24)
+    s = wl.scores_for(cfg)
+    eng.load_scores(s)
+    eng.load_profiles(inp.koff, inp.kx, inp.ky)
+    taus = [60.0, 120.0, 250.0]
+    params = [wl.with_span_epsilon(wl.truncated_params(), t, 4.0) for t in taus]
+    opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=0.0, kappa=cfg.kappa)
+    recs = eng.sweep_slo(inp.profile_index, inp.retained, taus, opt, params)
+    S = len(inp.retained)
+    assert len(recs) == S * len(taus)
+    prof = ProfileTable(inp.koff, inp.kx, inp.ky)
+    for ti, (t, p) in enumerate(zip(taus, params)):
+        one = eng.sweep(inp.profile_index, inp.retained,
+                        rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=t, kappa=cfg.kappa), p)
+        part = recs[ti * S:(ti + 1) * S]
+        assert np.array_equal(part["score"].view(np.int64), one["score"].view(np.int64))
+        assert np.array_equal(part["setup_id"], one["setup_id"])
+        assert (part["tau_ms"] == t).all()
+        op = Params(sub_max_iters=20, pga_max_iters=5, epsilon=p.epsilon)
+        for k in range(0, S, 7):
+            ref = oracle.evaluate_setup(s, prof, inp.profile_index[k], cfg.lambda_rps, t,
+                                        cfg.kappa, op)
+            assert bits(part[k]["score"]) == bits(ref["score"])
+            assert bits(part[k]["latency_ms"]) == bits(ref["latency_ms"])
+            assert int(part[k]["eval_passes"]) == ref["eval_passes"]
