@@ -154,10 +154,12 @@ int rw_set_stream(rw_ctx* ctx, void* cuda_stream);
 /* Device time of the last solver kernel launch (CUDA events on the launch stream). */
 int rw_last_kernel_ms(const rw_ctx* ctx, double* ms);
 
-/* Diagnostics: per-CTA cycle counters accumulated over the next launches
- * [0] pass phase 1, [1] pass phase 2, [2] pass walk, [3] polish, [4] polish window misses. */
+/* Diagnostics: counters summed over CTAs and over the launches since the last read
+ * (RW_PROF_SLOTS entries; see rw_solver.cuh `Prof` for the slot meanings: pass phase
+ * cycles, block classification counts, walker cycles, polish cycles and misses). */
+#define RW_PROF_SLOTS 16
 int rw_set_profiling(rw_ctx* ctx, int enable);
-int rw_get_profile(rw_ctx* ctx, int64_t* out8);
+int rw_get_profile(rw_ctx* ctx, int64_t* out);
 /* Diagnostics: `passes` eval passes at fixed prices on one CTA (per-pass cost probe). */
 int rw_bench_passes(rw_ctx* ctx, const double* targets, const double* alpha, int32_t passes,
                     double* g);

@@ -255,20 +255,20 @@ int rw_last_kernel_ms(const rw_ctx* ctx, double* ms) {
 int rw_set_profiling(rw_ctx* ctx, int enable) {
   if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
   CK(cudaSetDevice(ctx->device));
-  if (enable && !ctx->d_prof) CK(cudaMalloc(&ctx->d_prof, 8 * sizeof(long long)));
+  if (enable && !ctx->d_prof) CK(cudaMalloc(&ctx->d_prof, RW_PROF_SLOTS * sizeof(long long)));
   if (!enable && ctx->d_prof) {
     cudaFree(ctx->d_prof);
     ctx->d_prof = nullptr;
   }
-  if (ctx->d_prof) CK(cudaMemset(ctx->d_prof, 0, 8 * sizeof(long long)));
+  if (ctx->d_prof) CK(cudaMemset(ctx->d_prof, 0, RW_PROF_SLOTS * sizeof(long long)));
   return RW_OK;
 }
 
-int rw_get_profile(rw_ctx* ctx, int64_t* out8) {
+int rw_get_profile(rw_ctx* ctx, int64_t* out) {
   if (!ctx || !ctx->d_prof) return set_err(ctx, RW_ERR_VALIDATION, "profiling not enabled");
   CK(cudaStreamSynchronize(ctx->stream));
-  CK(cudaMemcpy(out8, ctx->d_prof, 8 * sizeof(long long), cudaMemcpyDeviceToHost));
-  CK(cudaMemset(ctx->d_prof, 0, 8 * sizeof(long long)));
+  CK(cudaMemcpy(out, ctx->d_prof, RW_PROF_SLOTS * sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->d_prof, 0, RW_PROF_SLOTS * sizeof(long long)));
   return RW_OK;
 }
 

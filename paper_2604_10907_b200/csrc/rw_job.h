@@ -56,7 +56,7 @@ struct Job {
   uint8_t* ws_model_of;
   uint64_t* ws_keys;
   unsigned long long* queue;
-  long long* prof_out;  // optional cycle counters [8] (debug)
+  long long* prof_out;  // optional diagnostics counters [RW_PROF_SLOTS]
 };
 
 // Host launcher (rw_kernels.cu). Returns a cudaError_t value.

@@ -67,24 +67,59 @@ __device__ __forceinline__ bool in_binade(double P, double E, int& e, int& neg) 
 }
 
 // ---------------------------------------------------------------------------------------
+// Exact-sum pieces (see Solver::pass_t).  A SAFE piece maps S -> S + u*q for S in binade
+// `key` (u = 2^(e-52)); a RAW piece is a row range the walker re-adds with IEEE adds.
+enum PieceKind { PIECE_SAFE = 1, PIECE_RAW = 2 };
+// Diagnostics slots (rw_get_profile): cycles are clock64 deltas of one thread per CTA.
+enum Prof {
+  PR_LOAD = 0,       // warp 0: load + argmax loop
+  PR_TOTBAR = 1,     // warp 0: waiting for the other blocks' totals
+  PR_EMPTY = 2,      // warp 0: waiting for the walker to free a slot
+  PR_POLISH = 3,     // polish_pass total
+  PR_PMISS = 4,      // polish coordinate selects that needed a second sweep
+  PR_PRADIX = 5,     // ... that needed the radix fallback
+  PR_WALK_WAIT = 6,  // walker: waiting for a tile's pieces
+  PR_WALK_BUSY = 7,  // walker: applying pieces
+  PR_FAST = 8,       // warp blocks summed as one SAFE piece
+  PR_SLOW = 9,       // warp blocks split into sub-segments
+  PR_RAW = 10,       // rows re-added by the walker
+  PR_PSWEEP = 11,    // polish sweeps (cycles)
+  PR_PSELECT = 12,   // polish candidate selection (cycles)
+  PR_PASS = 13,      // eval / fixed passes (cycles)
+  PR_REPAIR = 14,    // repair_counts (cycles)
+};
+struct Piece {
+  long long q;
+  int row, nrows;
+  int key;   // 2*e + sign (SAFE)
+  int kind;
+  int pad_[2];
+};
+
 // shared memory
 template <int MM, int L, int T>
 struct Smem {
-  static constexpr int R = L * T;       // rows per tile
   static constexpr int W = T / 32;      // warps
-  static constexpr int BPAD = L * T + (L * T) / 8 + 1;
-  double b[BPAD];                       // tile's b_j at k + k/8 (conflict-free both ways)
-  long long q0[T], q1[T];               // pieces: SAFE -> (Q0, Q1); RAW -> (start, count)
-  double scan_x[W], scan_y[W];
+  static constexpr int WP = W - 1;      // producer warps of a pass (warp W-1 walks)
+  static constexpr int BLK = 32 * L;    // rows per warp block
+  static constexpr int TILE = WP * BLK; // rows per tile
+  static constexpr int MAXP = L + 1;    // pieces per warp block
+  static constexpr int CAP = 4096;      // polish candidates kept in smem
+  Piece pieces[2][WP][MAXP];            // double-buffered by tile parity
+  int npieces[2][WP];
+  double tot_b[2][WP], tot_a[2][WP];    // per-block approximate sums (sum b, sum |b|)
+  union {
+    unsigned long long cand[CAP];       // polish candidates
+    double bscr[2][WP][BLK];            // a pass's b values (tile parity), for RAW re-adds
+  };
   unsigned hist[256];
-  unsigned char pkind[T];             // piece kind per slot (SAFE / RAW)
-  int wcnt[W];                         // pieces per warp
   // reduction scratch
   double red_d[W];
   int red_j[W];
   int red_v[W];
-  // pass outputs / carries
-  double S, P, A, tileP, tileA;
+  int red_i[W * 16];
+  // pass outputs
+  double S, mean_b;  // mean_b: last pass's sum / N (binade prediction)
   int counts[MM];
   // solve_dual state
   double alpha[MM], best_alpha[MM], polished[MM], zero[MM], c[MM], init[MM];
@@ -94,11 +129,11 @@ struct Smem {
   int target[MM], delta[MM];
   double gain[MM * MM];
   int witness[MM * MM];
-  // radix select
-  unsigned long long sel_prefix;
+  // selection
+  unsigned long long sel_prefix, sel_lo, sel_hi;
   int sel_k;
-  int cand_n, above_n;
-  double pol_delta;
+  int cand_n, cand_over;
+  double pol_delta[MM];
   // optimize_fractions state
   double w[MM], best_w[MM], warm[MM], grad[MM], step[MM], nextw[MM], tmp[MM];
   double best_obj;
@@ -116,7 +151,7 @@ struct Smem {
   double tr_best_lat, tr_best_score;
   // counters
   long long eval_passes, polish_passes, repair_calls;
-  long long prof[8];  // cycle counters (debug: Job.prof_out)
+  long long prof[RW_PROF_SLOTS];  // diagnostics counters (Job.prof_out)
   long long cur_item;
 };
 
@@ -215,7 +250,6 @@ __device__ inline bool project_simplex(int m, const double* v, double* w, double
 // The solver: all threads of the CTA execute every member function (uniform control
 // flow); scalar state lives in shared memory and is updated by thread 0 between barriers.
 enum PassMode { PASS_EVAL = 0, PASS_FIXED = 1 };
-enum PieceKind { PIECE_NONE = 0, PIECE_SAFE = 1, PIECE_RAW = 2 };
 
 // Shared memory is always reached through the extern __shared__ symbol so every access
 // compiles to LDS/STS (a reference member would decay to generic LD/ST).
@@ -229,7 +263,6 @@ __device__ __forceinline__ SMT& smem() {
 template <int MM, int L, int T>
 struct Solver {
   using SM = Smem<MM, L, T>;
-  static constexpr int R = SM::R;
   static constexpr int W = SM::W;
   static constexpr int NPK = (MM + 3) / 4;  // packed 16-bit count words
 
@@ -250,42 +283,63 @@ struct Solver {
   }
 
   // ---- one pass over the N x M matrix (score_dual.cpp:25-49) ------------------------
-  // PASS_EVAL : b_j = max_i (s_ji - alpha_i), arg = first max; counts; optional model_of.
+  // PASS_EVAL : b_j = max_i (s_ji - alpha_i), arg = first max (strict >, :38); counts;
+  //             optional model_of.
   // PASS_FIXED: b_j = s_j,mo[j] (mo == null -> column 0).
-  // Result: SMX.S = the reference's sequential FP64 sum of b_j, bit for bit.
+  // Result: SMX.S = the reference's sequential FP64 sum of b_j (:45), bit for bit.
   //
-  // Per tile of R = L*T rows:
-  //  phase 1 (coalesced, all threads): rows -> b_j into smem, argmax, packed counts.
-  //  phase 2 (all threads): thread t owns the contiguous chunk [t*L, t*L+L).  An
-  //    approximate block scan of (sum b, sum |b|) locates the binade of the running sum at
-  //    both chunk ends; a monotone chunk (all b >= 0 or all <= 0) whose two ends sit in
-  //    the same binade with margin E is SAFE and maps S -> S + u*Q_p (integer quanta,
-  //    two tracks for half-ulp ties).  Otherwise the chunk is RAW (exact IEEE adds).
-  //    A segmented warp scan composes runs of SAFE chunks of one binade into a single
-  //    piece, so each warp publishes ~1 piece (a few around binade crossings).
-  //  phase 3 (thread 0): apply the pieces in order to the exact running sum S.
-  // b_j of tile row k lives at k + k/8: coalesced writes in phase 1 and, for L = 24, the
-  // chunk reads of phase 2 (lane t at 27t + r) are bank-conflict free.
-  __device__ __forceinline__ static int bpos(int k) { return k + (k >> 3); }
+  // Layout: a tile is WP consecutive warp blocks of BLK = 32*L rows; producer warp w owns
+  // block w of every tile and reads it with coalesced, vectorised loads (lane l reads rows
+  // blk0 + 32 g + l, g < L), keeping b in registers.  Rows are therefore summed in
+  // block order, and inside a block in (g, lane) order — the reference's row order.
+  //
+  // Exact sum: while the running sum S stays in one binade [2^e, 2^(e+1))
+  // every add lands on the grid u = 2^(e-52), so a run of adds is S -> S + u * sum q_j with
+  // q_j = round(b_j / u) independent of S — except at exact half-ulp ties (parity-dependent).
+  // Each warp learns the approximate prefix before its block (one named barrier per tile
+  // exchanges block totals), proves with a rigorous error margin that every partial sum of
+  // the block stays in one binade, and publishes a single SAFE piece (e, Q); blocks near a
+  // binade crossing (or holding a tie, or with S ~ 0) are split into 32-row sub-segments,
+  // each SAFE or RAW.  A dedicated walker warp consumes the pieces in row order
+  // (double-buffered smem ring, named barriers), applying SAFE pieces as integer adds on
+  // the bit pattern of S and re-adding RAW rows with IEEE adds — the exact bits of the
+  // reference's left-to-right sum, overlapped with the next tile's loads.
+  static constexpr int WP = SM::WP, BLK = SM::BLK, TILE = SM::TILE, MAXP = SM::MAXP;
+  static constexpr int BAR_TOT = 1, BAR_FULL = 2, BAR_EMPTY = 4;  // named barrier ids
+  // Rows per load group (all loads of a group are in flight together).
+  static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : ((MM <= 16) ? 2 : 1));
+  static_assert(L % G == 0, "L must be a multiple of the load group");
 
-  // quanta of one |b| for u = 2^(base_sh - 1023 - 52): floor and half-way flag (exact, INT)
-  __device__ __forceinline__ static long long quanta_floor(double ab, int base_sh, bool& tie,
-                                                           bool& above) {
-    const unsigned long long B =
-        (unsigned long long)__double_as_longlong(ab) & 0x7fffffffffffffffull;
-    const int ebits = (int)(B >> 52);
-    const unsigned long long Mb =
-        (B & 0x000fffffffffffffull) | (ebits ? 0x0010000000000000ull : 0ull);
-    const int sh = base_sh - max(ebits, 1);
-    tie = false;
-    above = false;
-    if (sh <= 0) return (long long)(Mb << (-sh));
-    if (sh >= 54) return 0;
-    const unsigned long long rem = Mb & ((1ull << sh) - 1ull);
-    const unsigned long long half = 1ull << (sh - 1);
-    tie = (rem == half);
-    above = (rem > half);
-    return (long long)(Mb >> sh);
+  __device__ __forceinline__ static void bar_sync(int id, int cnt) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+  }
+  __device__ __forceinline__ static void bar_arrive(int id, int cnt) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+  }
+  // Warp sums evaluated in one fixed order and broadcast, so every lane holds the same bits.
+  __device__ __forceinline__ static double warp_sum_d(double x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
+    return __shfl_sync(FULL, x, 0);
+  }
+  __device__ __forceinline__ static long long warp_sum_ll(long long x) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
+    return x;  // lane 0
+  }
+  // Both ends of [lo, hi] in one normal binade with one sign.
+  __device__ __forceinline__ static bool range_binade(double lo, double hi, int& e, int& ng) {
+    int e1, n1;
+    if (!in_binade(lo, 0.0, e, ng) || !in_binade(hi, 0.0, e1, n1)) return false;
+    return e1 == e && n1 == ng;
+  }
+  // q = round(|b| / u) (RNE) with u = 1/scale and a half-way flag; |b| * scale < 2^52.
+  __device__ __forceinline__ static long long quanta(double b, double scale, bool& tie) {
+    const double y = fabs(b) * scale;
+    const double t = y + 0x1p52;
+    const long long q = __double_as_longlong(t) - 0x4330000000000000ll;
+    tie = tie || (fabs((t - 0x1p52) - y) == 0.5);
+    return (b < 0.0) ? -q : q;
   }
 
   __device__ void pass(int mode, const double* alpha_s, bool want_counts, uint8_t* mo_out,
@@ -303,105 +357,335 @@ struct Solver {
     }
   }
 
-  // Rows per load group in phase 1 (all loads of a group are in flight together).
-  static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : 2);
-  static_assert(L % G == 0, "L must be a multiple of the load group");
+  // b_j of one row (walker re-adds and fallbacks).
+  template <int MODE, bool FULLM>
+  __device__ __forceinline__ double row_b(int j, const double (&a)[MM], int m_,
+                                          const uint8_t* mo_in) const {
+    const double* row = jb.scores + (size_t)j * m_;
+    if (MODE == PASS_FIXED) return __ldg(row + (mo_in ? (int)mo_in[j] : 0));
+    double best = __dsub_rn(__ldg(row), a[0]);
+#pragma unroll
+    for (int i = 1; i < MM; ++i)
+      if (FULLM || i < m_) {
+        const double x = __dsub_rn(__ldg(row + i), a[i]);
+        if (x > best) best = x;
+      }
+    return best;
+  }
 
   template <int MODE, bool FULLM, bool WMO>
   __device__ __noinline__ void pass_t(const int n_, const double* alpha_s, const bool want_counts,
                                       uint8_t* mo_out, const uint8_t* mo_in) {
     const int tid_ = threadIdx.x, lane_ = tid_ & 31, wid_ = tid_ >> 5;
     const int m_ = FULLM ? MM : jb.m;
-    const double* __restrict__ sc = jb.scores;
     __syncthreads();  // callers may still be reading the previous pass's S / counts
     double a[MM];
 #pragma unroll
     for (int i = 0; i < MM; ++i) a[i] = (FULLM || i < m_) ? alpha_s[i] : 0.0;
     if (tid_ == 0) {
       SMX.S = 0.0;
-      SMX.P = 0.0;
-      SMX.A = 0.0;
       if (MODE == PASS_EVAL) SMX.eval_passes++;
     }
     if (tid_ < MM) SMX.counts[tid_] = 0;
     __syncthreads();
-    const bool vec2 = FULLM ? (MM % 2 == 0) : ((m_ & 1) == 0);
-    for (int base = 0; base < n_; base += R) {
-      const int len = min(R, n_ - base);
-      // -- phase 1 ----------------------------------------------------------------------
-      long long t_p1 = clock64();
-      unsigned long long pk[NPK];
-#pragma unroll
-      for (int q = 0; q < NPK; ++q) pk[q] = 0ull;
-      for (int r0 = 0; r0 < L; r0 += G) {
-        if (r0 * T >= len) break;  // block-uniform
-        double v[G][MODE == PASS_EVAL ? MM : 1];
-        int ag[G];
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const int kk = min((r0 + g) * T + tid_, len - 1);
-          const double* row = sc + (size_t)(base + kk) * m_;
-          if (MODE == PASS_EVAL) {
-            if (vec2) {
-              const double2* r2 = reinterpret_cast<const double2*>(row);
-#pragma unroll
-              for (int i = 0; i < MM / 2; ++i) {
-                if (FULLM || 2 * i < m_) {
-                  const double2 x = __ldg(r2 + i);
-                  v[g][2 * i] = x.x;
-                  v[g][2 * i + 1] = x.y;
-                } else {
-                  v[g][2 * i] = 0.0;
-                  v[g][2 * i + 1] = 0.0;
-                }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < MM; ++i) v[g][i] = (FULLM || i < m_) ? __ldg(row + i) : 0.0;
-            }
-          } else {
-            ag[g] = mo_in ? (int)mo_in[base + kk] : 0;
-            v[g][0] = __ldg(row + ag[g]);
-          }
-        }
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const int k = (r0 + g) * T + tid_;
-          double bj;
-          int arg;
-          if (MODE == PASS_EVAL) {
-            bj = __dsub_rn(v[g][0], a[0]);
-            arg = 0;
-#pragma unroll
-            for (int i = 1; i < MM; ++i) {
-              if (FULLM || i < m_) {
-                const double x = __dsub_rn(v[g][i], a[i]);
-                if (x > bj) {
-                  bj = x;
-                  arg = i;
-                }
+    const int ntiles = (n_ + TILE - 1) / TILE;
+    const long long t_pass = clock64();
+    if (wid_ == WP) {
+      walk<MODE, FULLM>(ntiles);
+    } else {
+      produce<MODE, FULLM, WMO>(n_, ntiles, a, m_, want_counts, mo_out, mo_in);
+    }
+    __syncthreads();
+    if (tid_ == 0) SMX.prof[PR_PASS] += clock64() - t_pass;
+  }
+
+  // Walker warp: applies the pieces of every tile in row order.  Pieces are fetched 32 at
+  // a time (one per lane) and broadcast; RAW rows are re-added by lane 0 from the tile's
+  // smem copy of b (double-buffered with the pieces), so the walk never touches HBM/L2.
+  template <int MODE, bool FULLM>
+  __device__ __forceinline__ void walk(int ntiles) {
+    const int lane_ = threadIdx.x & 31;
+    double S = 0.0;
+    long long raw_rows = 0;
+    for (int k = 0; k < ntiles; ++k) {
+      const int s = k & 1;
+      const long long t0 = clock64();
+      bar_sync(BAR_FULL + s, T);
+      const long long t1 = clock64();
+      for (int w2 = 0; w2 < WP; ++w2) {
+        const int np = SMX.npieces[s][w2];
+        const double* scr = SMX.bscr[s][w2];
+        const int blk0 = k * TILE + w2 * BLK;
+        for (int p0 = 0; p0 < np; p0 += 32) {
+          Piece mine;
+          if (p0 + lane_ < np) mine = SMX.pieces[s][w2][p0 + lane_];
+          const int cnt = min(32, np - p0);
+          for (int pp = 0; pp < cnt; ++pp) {
+            const long long q = __shfl_sync(FULL, mine.q, pp);
+            const int row = __shfl_sync(FULL, mine.row, pp);
+            const int nrows = __shfl_sync(FULL, mine.nrows, pp);
+            const int key = __shfl_sync(FULL, mine.key, pp);
+            const int kind = __shfl_sync(FULL, mine.kind, pp);
+            bool done = false;
+            if (kind == PIECE_SAFE) {
+              const long long bits = __double_as_longlong(S);
+              const int ex = (int)((bits >> 52) & 0x7ff) - 1023;
+              const int ng = bits < 0 ? 1 : 0;
+              if (ex == (key >> 1) && ng == (key & 1) && ex > -1000) {
+                S = apply_quanta(S, q, q);
+                done = true;
               }
             }
-          } else {
-            bj = v[g][0];
-            arg = ag[g];
-          }
-          if (k < len) {
-            SMX.b[bpos(k)] = bj;
-            if (want_counts) {
-              if (NPK == 1) {
-                pk[0] += 1ull << (arg * 16);
-              } else {
-#pragma unroll
-                for (int q = 0; q < NPK; ++q)
-                  pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+            if (!done) {  // RAW (or a SAFE piece whose premise failed): exact IEEE adds
+              raw_rows += nrows;
+              if (lane_ == 0) {
+                const double* src = scr + (row - blk0);
+#pragma unroll 8
+                for (int r = 0; r < nrows; ++r) S = __dadd_rn(S, src[r]);
               }
+              S = __shfl_sync(FULL, S, 0);
             }
-            if (WMO) mo_out[base + k] = (uint8_t)arg;
           }
         }
       }
-      if (want_counts) {
+      if (k + 2 < ntiles) bar_arrive(BAR_EMPTY + s, T);
+      if (lane_ == 0) {
+        SMX.prof[PR_WALK_WAIT] += t1 - t0;
+        SMX.prof[PR_WALK_BUSY] += clock64() - t1;
+      }
+    }
+    if (lane_ == 0) {
+      SMX.S = S;
+      SMX.mean_b = (n > 0) ? S / (double)n : 0.5;
+      SMX.prof[PR_RAW] += raw_rows;
+    }
+  }
+
+  // A block near a binade crossing (or holding a half-ulp tie): classify each 32-row
+  // sub-segment with its own margin; consecutive SAFE sub-segments of one binade merge.
+  // b comes from this warp's smem scratch.  Returns the number of pieces written.
+  __device__ __noinline__ int slow_block(const double* scr, const int blk0, const int n_,
+                                         double Pg, double Ag, Piece* out) {
+    const int lane_ = threadIdx.x & 31;
+    int np = 0;
+    long long Qrun = 0;
+    int run_key = 0, run_row = 0, run_rows = 0;
+    auto emit = [&](long long q, int row, int nrows, int key, int kind) {
+      if (lane_ == 0) {
+        Piece& pc = out[np];
+        pc.q = q;
+        pc.row = row;
+        pc.nrows = nrows;
+        pc.key = key;
+        pc.kind = kind;
+      }
+      ++np;
+    };
+#pragma unroll 1
+    for (int g = 0; g < L; ++g) {
+      const int row_g = blk0 + g * 32;
+      if (row_g >= n_) break;
+      const int cnt_g = min(32, n_ - row_g);
+      const double bg = scr[g * 32 + lane_];
+      const double sbg = warp_sum_d(bg), sag = warp_sum_d(fabs(bg));
+      const double Eg =
+          ((double)row_g + (double)cnt_g + 64.0) * 0x1p-51 * (Ag + sag) + sag * 0x1p-48;
+      int e = 0, ng = 0;
+      bool safe = range_binade(Pg - 0.5 * (sag - sbg) - Eg, Pg + 0.5 * (sag + sbg) + Eg, e, ng);
+      long long q = 0;
+      if (safe) {
+        bool tie = false;
+        q = quanta(bg, __longlong_as_double((long long)(52 - e + 1023) << 52), tie);
+        safe = !__any_sync(FULL, tie);
+      }
+      const int key = 2 * e + ng;
+      if (safe && run_rows > 0 && key == run_key) {
+        Qrun += q;
+        run_rows += cnt_g;
+      } else {
+        if (run_rows > 0) emit(warp_sum_ll(Qrun), run_row, run_rows, run_key, PIECE_SAFE);
+        if (safe) {
+          Qrun = q;
+          run_key = key;
+          run_row = row_g;
+          run_rows = cnt_g;
+        } else {
+          Qrun = 0;
+          run_rows = 0;
+          emit(0, row_g, cnt_g, 0, PIECE_RAW);
+        }
+      }
+      Pg += sbg;
+      Ag += sag;
+    }
+    if (run_rows > 0) emit(warp_sum_ll(Qrun), run_row, run_rows, run_key, PIECE_SAFE);
+    return np;
+  }
+
+  template <int MODE, bool FULLM, bool WMO>
+  __device__ __forceinline__ void produce(const int n_, const int ntiles, const double (&a)[MM],
+                                          const int m_, const bool want_counts, uint8_t* mo_out,
+                                          const uint8_t* mo_in) {
+    const int lane_ = threadIdx.x & 31, wid_ = threadIdx.x >> 5;
+    const double* __restrict__ sc = jb.scores;
+    const bool vec2 = FULLM ? (MM % 2 == 0) : ((m_ & 1) == 0);
+    double P = 0.0, A = 0.0;  // approximate (sum b, sum |b|) of every row before the tile
+    // estimated block total: predicts the binade before the block's prefix is known
+    double blk_est = (double)BLK * SMX.mean_b;
+    unsigned long long pk[NPK];
+#pragma unroll
+    for (int q = 0; q < NPK; ++q) pk[q] = 0ull;
+    for (int k = 0; k < ntiles; ++k) {
+      const int s = k & 1;
+      const int blk0 = k * TILE + wid_ * BLK;
+      const bool live = blk0 < n_;  // warp-uniform
+      const long long te = clock64();
+      if (k >= 2) bar_sync(BAR_EMPTY + s, T);  // the walker is done with tile k-2's slot
+      if (wid_ == 0 && lane_ == 0) SMX.prof[PR_EMPTY] += clock64() - te;
+      double* scr = SMX.bscr[s][wid_];
+      int e_pred = 0, ng_pred = 0;
+      const bool pred_ok = in_binade(P + (double)wid_ * blk_est, 0.0, e_pred, ng_pred);
+      const double scale =
+          pred_ok ? __longlong_as_double((long long)(52 - e_pred + 1023) << 52) : 1.0;
+      long long Q = 0;
+      bool tie = false;
+      double sb = 0.0, sa = 0.0;
+      const long long t0 = clock64();
+      // -- loads + priced argmax + speculative quanta -----------------------------------
+      if (live) {
+#pragma unroll 1
+        for (int g0 = 0; g0 < L; g0 += G) {
+          double v[G][MODE == PASS_EVAL ? MM : 1];
+          int ag[G];
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const int j = min(blk0 + (g0 + gg) * 32 + lane_, n_ - 1);
+            const double* row = sc + (size_t)j * m_;
+            if (MODE == PASS_EVAL) {
+              if (vec2) {
+                const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+                for (int i = 0; i < MM / 2; ++i) {
+                  if (FULLM || 2 * i < m_) {
+                    const double2 x = __ldg(r2 + i);
+                    v[gg][2 * i] = x.x;
+                    v[gg][2 * i + 1] = x.y;
+                  } else {
+                    v[gg][2 * i] = 0.0;
+                    v[gg][2 * i + 1] = 0.0;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < MM; ++i) v[gg][i] = (FULLM || i < m_) ? __ldg(row + i) : 0.0;
+              }
+            } else {
+              ag[gg] = mo_in ? (int)mo_in[j] : 0;
+              v[gg][0] = __ldg(row + ag[gg]);
+            }
+          }
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const int j = blk0 + (g0 + gg) * 32 + lane_;
+            double bj;
+            int arg = 0;
+            if (MODE == PASS_EVAL) {
+              bj = __dsub_rn(v[gg][0], a[0]);
+#pragma unroll
+              for (int i = 1; i < MM; ++i) {
+                if (FULLM || i < m_) {
+                  const double x = __dsub_rn(v[gg][i], a[i]);
+                  if (x > bj) {
+                    bj = x;
+                    arg = i;
+                  }
+                }
+              }
+            } else {
+              bj = v[gg][0];
+              arg = ag[gg];
+            }
+            const bool valid = j < n_;
+            bj = valid ? bj : 0.0;
+            scr[(g0 + gg) * 32 + lane_] = bj;
+            Q += quanta(bj, scale, tie);
+            sb += bj;
+            sa += fabs(bj);
+            if (valid) {
+              if (want_counts) {
+                if (NPK == 1) {
+                  pk[0] += 1ull << (arg * 16);
+                } else {
+#pragma unroll
+                  for (int q = 0; q < NPK; ++q)
+                    pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+                }
+              }
+              if (WMO) mo_out[j] = (uint8_t)arg;
+            }
+          }
+        }
+      }
+      // -- block totals -> approximate prefix before this block ------------------------
+      sb = warp_sum_d(sb);
+      sa = warp_sum_d(sa);
+      if (lane_ == 0) {
+        SMX.tot_b[s][wid_] = sb;
+        SMX.tot_a[s][wid_] = sa;
+      }
+      const long long t1 = clock64();
+      bar_sync(BAR_TOT, WP * 32);
+      const long long t2 = clock64();
+      double Pw = P, Aw = A;
+      const double P_prev = P;
+#pragma unroll 1
+      for (int w2 = 0; w2 < WP; ++w2) {
+        const double tb = SMX.tot_b[s][w2], ta = SMX.tot_a[s][w2];
+        if (w2 < wid_) {
+          Pw += tb;
+          Aw += ta;
+        }
+        P += tb;
+        A += ta;
+      }
+      blk_est = (P - P_prev) * (1.0 / WP);
+      if (wid_ == 0 && lane_ == 0) {
+        SMX.prof[PR_LOAD] += t1 - t0;
+        SMX.prof[PR_TOTBAR] += t2 - t1;
+      }
+      Piece* out = SMX.pieces[s][wid_];
+      int np = 0;
+      if (live) {
+        const int nrows = min(BLK, n_ - blk0);
+        // |approximate prefix - sequential sum| <= rows * 2^-52 * sum|b| (both orders); x2
+        const double E =
+            ((double)blk0 + (double)nrows + 64.0) * 0x1p-51 * (Aw + sa) + sa * 0x1p-48;
+        int e0, n0;
+        const bool fast =
+            range_binade(Pw - 0.5 * (sa - sb) - E, Pw + 0.5 * (sa + sb) + E, e0, n0) && pred_ok &&
+            e0 == e_pred && n0 == ng_pred && !__any_sync(FULL, tie);
+        if (fast) {  // whole block inside the predicted binade: one integer piece
+          Q = warp_sum_ll(Q);
+          if (lane_ == 0) {
+            Piece& pc = out[0];
+            pc.q = Q;
+            pc.row = blk0;
+            pc.nrows = nrows;
+            pc.key = 2 * e0 + n0;
+            pc.kind = PIECE_SAFE;
+          }
+          np = 1;
+          if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_FAST], 1ull);
+        } else {  // 32-row sub-segments from the smem copy of b
+          __syncwarp();
+          np = slow_block(scr, blk0, n_, Pw, Aw, out);
+          if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_SLOW], 1ull);
+        }
+      }
+      if (lane_ == 0) SMX.npieces[s][wid_] = np;
+      bar_arrive(BAR_FULL + s, T);
+      // per-model counts: 16-bit packed lanes, flushed before they can overflow
+      if (want_counts && ((k & 31) == 31 || k == ntiles - 1)) {
 #pragma unroll
         for (int q = 0; q < NPK; ++q) {
           unsigned long long x = pk[q];
@@ -415,215 +699,9 @@ struct Solver {
               if (i < m_ && cnt) atomicAdd(&SMX.counts[i], (int)cnt);
             }
           }
+          pk[q] = 0ull;
         }
       }
-      __syncthreads();
-      long long t_p2 = clock64();
-      if (tid_ == 0) SMX.prof[0] += t_p2 - t_p1;
-      // -- phase 2 ----------------------------------------------------------------------
-      static_assert(L % 8 == 0, "chunk addressing assumes L % 8 == 0");
-      const int c0 = tid_ * L;
-      const int cnt = max(0, min(L, len - c0));
-      const double* bch = SMX.b + bpos(c0);
-      double bl[L];
-      double ps = 0.0;
-      unsigned orhi = 0u, andhi = 0xffffffffu;
-#pragma unroll
-      for (int r = 0; r < L; ++r) {
-        bl[r] = 0.0;
-        if (r < cnt) {
-          bl[r] = bch[r + (r >> 3)];
-          ps += bl[r];
-          const unsigned hi = (unsigned)__double2hiint(bl[r]);
-          orhi |= hi;
-          andhi &= hi;
-        }
-      }
-      const bool allpos = (orhi >> 31) == 0u;   // every b has its sign bit clear (incl. +0)
-      const bool allneg = (andhi >> 31) != 0u;  // every b has its sign bit set
-      double pa;
-      if (allpos) pa = ps;
-      else if (allneg) pa = -ps;
-      else {
-        pa = 0.0;
-#pragma unroll
-        for (int r = 0; r < L; ++r) pa += fabs(bl[r]);
-      }
-      // block exclusive scan of (ps, pa) — approximate; used only behind a margin
-      double ix = ps, iy = pa;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        double tx = __shfl_up_sync(FULL, ix, off), ty = __shfl_up_sync(FULL, iy, off);
-        if (lane_ >= off) {
-          ix += tx;
-          iy += ty;
-        }
-      }
-      if (lane_ == 31) {
-        SMX.scan_x[wid_] = ix;
-        SMX.scan_y[wid_] = iy;
-      }
-      __syncthreads();
-      if (wid_ == 0) {  // exclusive scan of the W warp totals (+ the tile carry)
-        double wx = (lane_ < W) ? SMX.scan_x[lane_] : 0.0;
-        double wy = (lane_ < W) ? SMX.scan_y[lane_] : 0.0;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          double tx = __shfl_up_sync(FULL, wx, off), ty = __shfl_up_sync(FULL, wy, off);
-          if (lane_ >= off) {
-            wx += tx;
-            wy += ty;
-          }
-        }
-        const double ox = __shfl_up_sync(FULL, wx, 1), oy = __shfl_up_sync(FULL, wy, 1);
-        const double cp = SMX.P, ca = SMX.A;
-        if (lane_ < W) {
-          SMX.scan_x[lane_] = cp + (lane_ ? ox : 0.0);
-          SMX.scan_y[lane_] = ca + (lane_ ? oy : 0.0);
-        }
-        if (lane_ == W - 1) {
-          SMX.tileP = wx;
-          SMX.tileA = wy;
-        }
-      }
-      double ex = __shfl_up_sync(FULL, ix, 1), ey = __shfl_up_sync(FULL, iy, 1);
-      if (lane_ == 0) {
-        ex = 0.0;
-        ey = 0.0;
-      }
-      __syncthreads();
-      const double P0 = SMX.scan_x[wid_] + ex;
-      const double A0 = SMX.scan_y[wid_] + ey;
-      const long long jg = (long long)base + c0;
-      int kind = (cnt > 0) ? PIECE_RAW : PIECE_NONE;
-      int e_ref = 0, neg_ref = 0;
-      if (cnt > 0) {
-        if (allpos || allneg) {
-          // S_j is monotone across the chunk: both ends in one binade => all inside.
-          const double P1 = P0 + ps, A1 = A0 + pa;
-          const double E = (double)(jg + cnt + 64) * 0x1p-51 * A1;
-          int e1, n1;
-          if (in_binade(P0, E, e_ref, neg_ref) && in_binade(P1, E, e1, n1) && e1 == e_ref &&
-              n1 == neg_ref)
-            kind = PIECE_SAFE;
-        } else {
-          double P = P0, A = A0;
-          bool ok = true;
-#pragma unroll
-          for (int r = 0; r <= L; ++r) {
-            if (r <= cnt && ok) {
-              const double x = (r < cnt) ? bl[r] : 0.0;
-              const double E = (double)(jg + r + 64) * 0x1p-51 * (A + fabs(x));
-              int e, ng;
-              if (!in_binade(P, E, e, ng)) ok = false;
-              else if (r == 0) {
-                e_ref = e;
-                neg_ref = ng;
-              } else if (e != e_ref || ng != neg_ref) ok = false;
-              P += x;
-              A += fabs(x);
-            }
-          }
-          if (ok) kind = PIECE_SAFE;
-        }
-      }
-      long long Q0 = 0, Q1 = 0;
-      if (kind == PIECE_SAFE) {
-        // q_j = round(b_j / u), u = 2^(e-52).  Monotone fast path in FP64: y = |b| * 2^(52-e)
-        // is exact and < 2^52 (S and S + b share the binade), so t = y + 2^52 rounds y to
-        // the integer grid (RNE) and bits(t) - bits(2^52) is that integer; a half-way
-        // y (|t - 2^52 - y| == 1/2) is a tie whose rounding depends on S — slow path.
-        bool tie_any = false;
-        if (allpos || allneg) {
-          const double scale = __longlong_as_double((long long)(52 - e_ref + 1023) << 52);
-          unsigned long long acc = 0ull;
-#pragma unroll
-          for (int r = 0; r < L; ++r) {
-            if (r < cnt) {
-              const double y = fabs(bl[r]) * scale;
-              const double t = y + 0x1p52;
-              acc += (unsigned long long)__double_as_longlong(t) - 0x4330000000000000ull;
-              tie_any |= (fabs((t - 0x1p52) - y) == 0.5);
-            }
-          }
-          Q0 = allpos ? (long long)acc : -(long long)acc;
-          Q1 = Q0;
-        }
-        if (!(allpos || allneg) || tie_any) {  // general: signed b, two parity tracks
-          const int base_sh = 1023 + e_ref;
-          Q0 = 0;
-          Q1 = 0;
-          for (int r = 0; r < cnt; ++r) {
-            const double x = bch[r + (r >> 3)];
-            bool tie, above;
-            const long long q = quanta_floor(x, base_sh, tie, above);
-            const bool negb = x < 0.0;
-            if (tie) {  // |x|/u = q + 1/2; RNE picks the neighbour leaving S/u even
-              const long long lo = negb ? -q - 1 : q;
-              Q0 += ((Q0 + lo) & 1) ? lo + 1 : lo;
-              Q1 += ((1 + Q1 + lo) & 1) ? lo + 1 : lo;
-            } else {
-              const long long qq = q + (above ? 1 : 0);
-              Q0 += negb ? -qq : qq;
-              Q1 += negb ? -qq : qq;
-            }
-          }
-        }
-      }
-      // segmented warp scan: compose consecutive SAFE chunks of one binade
-      const int key = (kind == PIECE_SAFE) ? (e_ref * 2 + neg_ref) : -100000 - lane_;
-      const int pkey = __shfl_up_sync(FULL, key, 1);
-      const bool head = (lane_ == 0) || kind != PIECE_SAFE || pkey != key;
-      {
-        bool f = head;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          long long o0 = __shfl_up_sync(FULL, Q0, d), o1 = __shfl_up_sync(FULL, Q1, d);
-          bool of = __shfl_up_sync(FULL, f, d);
-          if (lane_ >= d && !f) {
-            long long n0 = o0 + ((o0 & 1) ? Q1 : Q0);
-            long long n1 = o1 + (((1 + o1) & 1) ? Q1 : Q0);
-            Q0 = n0;
-            Q1 = n1;
-            f = of;
-          }
-        }
-      }
-      const bool nhead = __shfl_down_sync(FULL, head, 1);
-      const bool tail = (kind != PIECE_NONE) && (lane_ == 31 || nhead);
-      const unsigned tmask = __ballot_sync(FULL, tail);
-      if (tail) {
-        const int slot = wid_ * 32 + __popc(tmask & ((1u << lane_) - 1u));
-        SMX.pkind[slot] = (unsigned char)kind;
-        SMX.q0[slot] = (kind == PIECE_SAFE) ? Q0 : (long long)c0;
-        SMX.q1[slot] = (kind == PIECE_SAFE) ? Q1 : (long long)cnt;
-      }
-      if (lane_ == 0) SMX.wcnt[wid_] = __popc(tmask);
-      __syncthreads();
-      long long t_p3 = clock64();
-      if (tid_ == 0) SMX.prof[1] += t_p3 - t_p2;
-      // -- phase 3: ordered walk over the pieces (one thread) ----------------------------
-      if (tid_ == 0) {
-        double S = SMX.S;
-        for (int w = 0; w < W; ++w) {
-          const int np = SMX.wcnt[w];
-          for (int p = 0; p < np; ++p) {
-            const int slot = w * 32 + p;
-            const long long x0 = SMX.q0[slot], x1 = SMX.q1[slot];
-            if (SMX.pkind[slot] == PIECE_SAFE) {
-              S = apply_quanta(S, x0, x1);
-            } else {
-              const int k0 = (int)x0, rc = (int)x1;
-              for (int r = 0; r < rc; ++r) S = __dadd_rn(S, SMX.b[bpos(k0 + r)]);
-            }
-          }
-        }
-        SMX.S = S;
-        SMX.P += SMX.tileP;
-        SMX.A += SMX.tileA;
-      }
-      __syncthreads();
-      if (tid_ == 0) SMX.prof[2] += clock64() - t_p3;
     }
   }
 
@@ -635,7 +713,7 @@ struct Solver {
     return __ddiv_rn(g, (double)n);  // every thread computes the same value
   }
 
-  // ---- radix select: k-th largest key among keys[0..n) (nth_element, :71-72) ----------
+  // ---- radix select over smem candidates / recomputed keys -----------------------------
   __device__ __forceinline__ void hist_add(bool ok, unsigned d) {
     unsigned act = __activemask();
     unsigned key = ok ? d : 0xffffffffu;
@@ -673,22 +751,218 @@ struct Solver {
     }
   }
 
+  // Block sum of an int (all threads get it).
+  __device__ int block_sum_i(int x, int slot) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(FULL, x, off);
+    if (lane == 0) SMX.red_i[slot * W + wid] = x;
+    __syncthreads();
+    int t = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < W; ++w2) t += SMX.red_i[slot * W + w2];
+    return t;
+  }
+
+  // Polish sweep over every row: b_j = s_ji - max_{q != i}(s_jq - a_q) handed to f.
+  // The coordinate is a template constant for full-width rows (no per-model selects).
+  template <bool FULLM, int I, class F>
+  __device__ __forceinline__ void polish_sweep_t(int i_rt, const double (&a)[MM], F& f) {
+    const int m_ = FULLM ? MM : jb.m;
+    const int i = (I >= 0) ? I : i_rt;
+    const bool vec2 = FULLM ? (MM % 2 == 0) : ((m_ & 1) == 0);
+    const double* __restrict__ sc = jb.scores;
+    constexpr int GP = (MM <= 4) ? 4 : ((MM <= 8) ? 2 : 1);
+    for (int base = 0; base < n; base += GP * T) {
+      double v[GP][MM];
+#pragma unroll
+      for (int gg = 0; gg < GP; ++gg) {
+        const int j = min(base + gg * T + tid, n - 1);
+        const double* row = sc + (size_t)j * m_;
+        if (vec2) {
+          const double2* r2 = reinterpret_cast<const double2*>(row);
+#pragma unroll
+          for (int q = 0; q < MM / 2; ++q) {
+            if (FULLM || 2 * q < m_) {
+              const double2 x = __ldg(r2 + q);
+              v[gg][2 * q] = x.x;
+              v[gg][2 * q + 1] = x.y;
+            } else {
+              v[gg][2 * q] = 0.0;
+              v[gg][2 * q + 1] = 0.0;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < MM; ++q) v[gg][q] = (FULLM || q < m_) ? __ldg(row + q) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int gg = 0; gg < GP; ++gg) {
+        const int j = base + gg * T + tid;
+        double rest = -CUDART_INF, vi = 0.0;
+#pragma unroll
+        for (int q = 0; q < MM; ++q) {
+          if (FULLM || q < m_) {
+            if (q == i) vi = v[gg][q];
+            else rest = smax(rest, __dsub_rn(v[gg][q], a[q]));
+          }
+        }
+        f(j < n, __dsub_rn(vi, rest));
+      }
+    }
+  }
+  template <bool FULLM, class F>
+  __device__ __forceinline__ void polish_sweep(int i, const double (&a)[MM], F& f) {
+    if constexpr (FULLM && MM <= 8) {
+      switch (i) {
+        case 0: polish_sweep_t<FULLM, 0>(i, a, f); return;
+        case 1: polish_sweep_t<FULLM, 1 % MM>(i, a, f); return;
+        case 2: polish_sweep_t<FULLM, 2 % MM>(i, a, f); return;
+        case 3: polish_sweep_t<FULLM, 3 % MM>(i, a, f); return;
+        case 4: polish_sweep_t<FULLM, 4 % MM>(i, a, f); return;
+        case 5: polish_sweep_t<FULLM, 5 % MM>(i, a, f); return;
+        case 6: polish_sweep_t<FULLM, 6 % MM>(i, a, f); return;
+        default: polish_sweep_t<FULLM, 7 % MM>(i, a, f); return;
+      }
+    } else {
+      polish_sweep_t<FULLM, -1>(i, a, f);
+    }
+  }
+
+  // Append keys in [lo, hi] to SMX.cand (warp-aggregated); cand_over flags overflow.
+  __device__ __forceinline__ void gather(bool in, unsigned long long key) {
+    const unsigned inm = __ballot_sync(FULL, in);
+    if (inm) {
+      const int leader = __ffs(inm) - 1;
+      int basepos = 0;
+      if (lane == leader) basepos = atomicAdd(&SMX.cand_n, __popc(inm));
+      basepos = __shfl_sync(FULL, basepos, leader);
+      if (in) {
+        const int pos = basepos + __popc(inm & ((1u << lane) - 1u));
+        if (pos < SM::CAP) SMX.cand[pos] = key;
+      }
+    }
+  }
+
+  // r-th largest (1-based) among the nc <= CAP keys in SMX.cand -> SMX.sel_prefix.
+  __device__ void select_in_cand(int nc, int r) {
+    if (nc <= 128) {  // rank by comparison: one barrier
+      for (int x = tid; x < nc; x += T) {
+        const unsigned long long kx = SMX.cand[x];
+        int gt = 0, ge = 0;
+        for (int y = 0; y < nc; ++y) {
+          const unsigned long long ky = SMX.cand[y];
+          gt += ky > kx;
+          ge += ky >= kx;
+        }
+        if (gt < r && r <= ge) SMX.sel_prefix = kx;  // equal keys write equal values
+      }
+      __syncthreads();
+      return;
+    }
+    if (tid == 0) {
+      SMX.sel_prefix = 0ull;
+      SMX.sel_k = r;
+    }
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      __syncthreads();
+      if (tid < 256) SMX.hist[tid] = 0u;
+      __syncthreads();
+      const unsigned long long hi = (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8));
+      for (int q = tid; q < nc; q += T) {
+        const unsigned long long key = SMX.cand[q];
+        hist_add(shift == 56 || (key >> (shift + 8)) == hi, (unsigned)((key >> shift) & 0xffull));
+      }
+      __syncthreads();
+      select_digit(shift);
+    }
+    __syncthreads();
+  }
+
+  static constexpr int NSH = 5;  // nested windows a_i +- d * 8^s (value space)
+  static_assert(2 * NSH <= 16, "red_i stride");
+  struct CountWin {
+    double lo[NSH], hi[NSH];
+    int gt[NSH], lt[NSH];
+    Solver* s;
+    __device__ __forceinline__ void operator()(bool ok, double bv) {
+#pragma unroll
+      for (int q = 0; q < NSH; ++q) {
+        gt[q] += (ok && bv > hi[q]) ? 1 : 0;
+        lt[q] += (ok && bv < lo[q]) ? 1 : 0;
+      }
+      const bool in = ok && bv >= lo[0] && bv <= hi[0];
+      s->gather(in, in ? dkey(bv) : 0ull);
+    }
+  };
+  // Block sums of NSH*2 ints (one barrier).
+  __device__ void block_sum_counts(int (&gt)[NSH], int (&lt)[NSH]) {
+#pragma unroll
+    for (int q = 0; q < NSH; ++q) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        gt[q] += __shfl_down_sync(FULL, gt[q], off);
+        lt[q] += __shfl_down_sync(FULL, lt[q], off);
+      }
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < NSH; ++q) {
+        SMX.red_i[wid * 16 + q] = gt[q];
+        SMX.red_i[wid * 16 + NSH + q] = lt[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NSH; ++q) {
+      gt[q] = lt[q] = 0;
+      for (int w2 = 0; w2 < W; ++w2) {
+        gt[q] += SMX.red_i[w2 * 16 + q];
+        lt[q] += SMX.red_i[w2 * 16 + NSH + q];
+      }
+    }
+  }
+  struct GatherRange {  // keys in [lo, hi]
+    unsigned long long lo, hi;
+    Solver* s;
+    __device__ __forceinline__ void operator()(bool ok, double bv) {
+      const unsigned long long key = dkey(bv);
+      s->gather(ok && key >= lo && key <= hi, key);
+    }
+  };
+  struct RadixRange {  // histogram of one digit of the keys in [lo, hi] matching the prefix
+    unsigned long long lo, hi, pre;
+    int shift;
+    Solver* s;
+    __device__ __forceinline__ void operator()(bool ok, double bv) {
+      const unsigned long long key = dkey(bv);
+      const bool in = ok && key >= lo && key <= hi &&
+                      (shift == 56 || (key >> (shift + 8)) == pre);
+      s->hist_add(in, (unsigned)((key >> shift) & 0xffull));
+    }
+  };
+
   // ---- polish_pass (score_dual.cpp:54-76) on SMX.polished --------------------------------
-  // For coordinate i the new price is the k-th largest b_j = s_ji - max_{k!=i}(s_jk - a_k),
-  // k = ceil(c_i - 1e-9) (nth_element, :69-72).  Near the optimum that value sits close to
-  // the current a_i, so one sweep counts the keys above a window [a_i - d, a_i + d] and
-  // gathers the keys inside it into shared memory; the k-th largest is then selected among
-  // the few candidates (radix select in smem).  If the window misses or overflows, an exact
-  // 8-digit radix select over all N keys (written during the same sweep) is the fallback.
-  // d adapts per CTA; the result is exact either way.
+  // Coordinate i's new price is the k-th largest b_j = s_ji - max_{q != i}(s_jq - a_q),
+  // k = ceil(c_i - 1e-9) clamped to [1, N] (nth_element, :69-72).  Near the optimum that
+  // value sits close to a_i, so one sweep counts keys against two nested windows around
+  // a_i (+-d, +-64d) and gathers the inner window's keys into smem; the k-th largest is then
+  // selected among those candidates.  A miss names the shell holding it, which a second
+  // sweep gathers; only an overfull shell falls back to an 8-round radix select over
+  // recomputed keys.  No key ever leaves the SM; d adapts per coordinate; exact either way.
   __device__ __noinline__ void polish_pass() {
-    constexpr int CAP = SM::BPAD;
+    if (m == MM) polish_t<true>();
+    else polish_t<false>();
+  }
+
+  template <bool FULLM>
+  __device__ void polish_t() {
     const long long t_pol = clock64();
     if (tid == 0) {
       SMX.max_delta = 0.0;
       SMX.polish_passes++;
     }
-    unsigned long long* cand = reinterpret_cast<unsigned long long*>(SMX.b);
     for (int i = 0; i < m; ++i) {
       __syncthreads();
       double a[MM];
@@ -697,97 +971,109 @@ struct Solver {
       const double ci = SMX.c[i];
       int k = ci > 1e-12 ? (int)ceil(__dsub_rn(ci, 1e-9)) : 1;
       k = max(1, min(k, n));
-      const double ai = SMX.polished[i], dl = SMX.pol_delta;
-      const unsigned long long klo = dkey(ai - dl), khi = dkey(ai + dl);
-      if (tid < 256) SMX.hist[tid] = 0u;
-      if (tid == 0) {
-        SMX.sel_prefix = 0ull;
-        SMX.sel_k = k;
-        SMX.cand_n = 0;
-        SMX.above_n = 0;
-      }
-      __syncthreads();
-      int my_above = 0;
-      for (int j = tid; j < n; j += T) {
-        const double* row = jb.scores + (size_t)j * m;
-        double rest = -CUDART_INF;
-        double vi = 0.0;
+      const double ai = a[i], dl = SMX.pol_delta[i];
+      CountWin cw;
+      {
+        double r = dl;
 #pragma unroll
-        for (int q = 0; q < MM; ++q) {
-          if (q < m) {
-            double v = __ldg(row + q);
-            if (q == i) vi = v;
-            else rest = smax(rest, __dsub_rn(v, a[q]));
-          }
-        }
-        const unsigned long long key = dkey(__dsub_rn(vi, rest));
-        keys[j] = key;
-        my_above += (key > khi) ? 1 : 0;
-        const bool in = (key >= klo) && (key <= khi);
-        const unsigned act = __activemask();
-        const unsigned inm = __ballot_sync(act, in);
-        if (inm) {
-          const int leader = __ffs(inm) - 1;
-          int basepos = 0;
-          if (lane == leader) basepos = atomicAdd(&SMX.cand_n, __popc(inm));
-          basepos = __shfl_sync(act, basepos, leader);
-          if (in) {
-            const int pos = basepos + __popc(inm & ((1u << lane) - 1u));
-            if (pos < CAP) cand[pos] = key;
-          }
+        for (int q = 0; q < NSH; ++q, r *= 8.0) {
+          cw.lo[q] = ai - r;
+          cw.hi[q] = ai + r;
+          cw.gt[q] = cw.lt[q] = 0;
         }
       }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) my_above += __shfl_down_sync(FULL, my_above, off);
-      if (lane == 0 && my_above) atomicAdd(&SMX.above_n, my_above);
+      cw.s = this;
+      if (tid == 0) SMX.cand_n = 0;
       __syncthreads();
-      const int nc = SMX.cand_n, na = SMX.above_n;
-      const bool win = (nc <= CAP) && (na < k) && (k <= na + nc);
-      if (win) {
-        if (tid == 0) SMX.sel_k = k - na;
-        for (int shift = 56; shift >= 0; shift -= 8) {
-          __syncthreads();
-          if (tid < 256) SMX.hist[tid] = 0u;
-          __syncthreads();
-          const unsigned long long hi = (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8));
-          for (int q = tid; q < nc; q += T) {
-            const unsigned long long key = cand[q];
-            hist_add(shift == 56 || (key >> (shift + 8)) == hi,
-                     (unsigned)((key >> shift) & 0xffull));
+      const long long ts0 = clock64();
+      polish_sweep<FULLM>(i, a, cw);
+      block_sum_counts(cw.gt, cw.lt);
+      const int nin = n - cw.gt[0] - cw.lt[0];
+      int nc = SMX.cand_n;
+      const long long ts1 = clock64();
+      int miss = 0;
+      const bool gt_k_in = cw.gt[0] < k && k <= cw.gt[0] + nin;  // k-th largest inside +-d
+      if (gt_k_in && nc <= SM::CAP) {
+        select_in_cand(nc, k - cw.gt[0]);
+      } else {  // the shell holding the k-th largest, scanning shells from the top
+        miss = 1;
+        unsigned long long lo = 0ull, hi = ~0ull;
+        int r = k, cnt = 0, above = 0;
+        for (int z = 0; z < 2 * NSH + 1; ++z) {
+          int c;
+          // b > x  <=>  dkey(b) > dkey(x): value-space shells as key ranges
+          if (z < NSH) {  // above shells: (hi[q], hi[q+1]] from the outside in
+            const int q = NSH - 1 - z;
+            c = (q == NSH - 1 ? cw.gt[q] : cw.gt[q] - cw.gt[q + 1]);
+            lo = dkey(cw.hi[q]) + 1;
+            hi = (q == NSH - 1) ? ~0ull : dkey(cw.hi[q + 1]);
+          } else if (z == NSH) {
+            c = nin;
+            lo = dkey(cw.lo[0]);
+            hi = dkey(cw.hi[0]);
+          } else {  // below shells: [lo[q+1], lo[q]) from the inside out
+            const int q = z - NSH - 1;
+            c = (q == NSH - 1 ? cw.lt[q] : cw.lt[q] - cw.lt[q + 1]);
+            lo = (q == NSH - 1) ? 0ull : dkey(cw.lo[q + 1]);
+            hi = dkey(cw.lo[q]) - 1;
           }
-          __syncthreads();
-          select_digit(shift);
+          if (above + c >= k) {
+            r = k - above;
+            cnt = c;
+            break;
+          }
+          above += c;
         }
-      } else {
-        for (int shift = 56; shift >= 0; shift -= 8) {
+        if (cnt <= SM::CAP) {
+          miss = 2;
           __syncthreads();
-          if (tid < 256) SMX.hist[tid] = 0u;
+          if (tid == 0) SMX.cand_n = 0;
           __syncthreads();
-          const unsigned long long hi = (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8));
-          for (int j = tid; j < n; j += T) {
-            const unsigned long long key = keys[j];
-            hist_add(shift == 56 || (key >> (shift + 8)) == hi,
-                     (unsigned)((key >> shift) & 0xffull));
+          GatherRange gr{lo, hi, this};
+          polish_sweep<FULLM>(i, a, gr);
+          __syncthreads();
+          nc = SMX.cand_n;
+          select_in_cand(nc, r);
+        } else {  // radix select over recomputed keys of the shell
+          miss = 3;
+          if (tid == 0) {
+            SMX.sel_prefix = 0ull;
+            SMX.sel_k = r;
+          }
+          for (int shift = 56; shift >= 0; shift -= 8) {
+            __syncthreads();
+            if (tid < 256) SMX.hist[tid] = 0u;
+            __syncthreads();
+            RadixRange rr{lo, hi, (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8)), shift,
+                          this};
+            polish_sweep<FULLM>(i, a, rr);
+            __syncthreads();
+            select_digit(shift);
           }
           __syncthreads();
-          select_digit(shift);
         }
       }
-      __syncthreads();
       if (tid == 0) {
+        SMX.prof[PR_PSWEEP] += ts1 - ts0;
+        SMX.prof[PR_PSELECT] += clock64() - ts1;
         const double next = dkey_inv(SMX.sel_prefix);
         SMX.max_delta = smax(SMX.max_delta, fabs(__dsub_rn(next, SMX.polished[i])));
         SMX.polished[i] = next;
-        if (nc > CAP) SMX.pol_delta *= 0.125;
-        else if (!win) SMX.pol_delta = fmin(SMX.pol_delta * 8.0, 4.0);
-        else if (nc > CAP / 4) SMX.pol_delta *= 0.5;
-        if (!win) SMX.prof[4]++;
+        // adapt the window: aim for a hit with a few hundred candidates
+        double d = SMX.pol_delta[i];
+        if (miss && nin > SM::CAP && gt_k_in) d *= 0.125;  // the window itself overflowed
+        else if (miss) d = fmin(fmax(d * 2.0, 1.5 * fabs(__dsub_rn(next, ai))), 4.0);
+        else if (nc > 512) d *= 0.25;
+        else if (nc > 128) d *= 0.5;
+        else if (nc < 24) d = fmin(d * 2.0, 4.0);
+        SMX.pol_delta[i] = fmax(d, 1e-300);
+        if (miss) SMX.prof[PR_PMISS]++;
+        if (miss == 3) SMX.prof[PR_PRADIX]++;
       }
     }
     __syncthreads();
-    if (tid == 0) SMX.prof[3] += clock64() - t_pol;
+    if (tid == 0) SMX.prof[PR_POLISH] += clock64() - t_pol;
   }
-
   // ---- block argmin / argmax helpers (lexicographic with index tie-break) ------------
   // returns winner to all threads via smem: (val, j, v)
   __device__ void block_argmin(double& val, int& j, int& v) {
@@ -861,6 +1147,7 @@ struct Solver {
 
   // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
+    const long long t_rep = clock64();
     if (tid == 0) {
       SMX.repair_calls++;
       for (int i = 0; i < m; ++i) SMX.delta[i] = SMX.counts[i] - SMX.target[i];
@@ -995,6 +1282,7 @@ struct Solver {
     __syncthreads();
     // exact sequential mean of the repaired assignment (:182-184)
     pass(PASS_FIXED, SMX.zero, false, nullptr, mo);
+    if (tid == 0) SMX.prof[PR_REPAIR] += clock64() - t_rep;
     return __ddiv_rn(SMX.S, (double)n);
   }
 
@@ -1277,8 +1565,9 @@ struct Solver {
       SMX.eval_passes = 0;
       SMX.polish_passes = 0;
       SMX.repair_calls = 0;
-      SMX.pol_delta = 1e-3;
-      for (int i = 0; i < 8; ++i) SMX.prof[i] = 0;
+      for (int i = 0; i < MM; ++i) SMX.pol_delta[i] = 1e-3;
+      SMX.mean_b = 0.5;
+      for (int i = 0; i < RW_PROF_SLOTS; ++i) SMX.prof[i] = 0;
       for (int i = 0; i < MM; ++i) SMX.zero[i] = 0.0;
     }
     __syncthreads();
@@ -1353,7 +1642,7 @@ __global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kern
       if (k >= jb.n_items) break;
       s.evaluate_setup(k, jb.records + item);
       if (tid == 0 && jb.prof_out)
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < RW_PROF_SLOTS; ++i)
           atomicAdd((unsigned long long*)jb.prof_out + i, (unsigned long long)sm.prof[i]);
       if (tid == 0 && sm.status && jb.status_out) atomicCAS(jb.status_out, 0, sm.status);
     }
@@ -1468,7 +1757,7 @@ __global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kern
   __syncthreads();
   if (tid == 0 && sm.status && jb.status_out) atomicCAS(jb.status_out, 0, sm.status);
   if (tid == 0 && jb.prof_out)
-    for (int i = 0; i < 8; ++i) atomicAdd((unsigned long long*)jb.prof_out + i, (unsigned long long)sm.prof[i]);
+    for (int i = 0; i < RW_PROF_SLOTS; ++i) atomicAdd((unsigned long long*)jb.prof_out + i, (unsigned long long)sm.prof[i]);
 }
 
 }  // namespace rw
