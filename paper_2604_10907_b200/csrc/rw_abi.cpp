@@ -313,8 +313,8 @@ int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* dev) 
   if (m > RW_MAX_MODELS)
     return set_err(ctx, RW_ERR_UNSUPPORTED,
                    "rw_b200 supports at most " + std::to_string(RW_MAX_MODELS) + " models");
-  if ((reinterpret_cast<uintptr_t>(dev) & 15u) != 0)
-    return set_err(ctx, RW_ERR_VALIDATION, "device score matrix must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(dev) & 31u) != 0)  // 256-bit row loads
+    return set_err(ctx, RW_ERR_VALIDATION, "device score matrix must be 32-byte aligned");
   ctx->d_scores = dev;
   ctx->n = n;
   ctx->m = m;

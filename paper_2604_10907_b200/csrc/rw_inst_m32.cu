@@ -1,2 +1,2 @@
 #include "rw_inst.cuh"
-RW_INSTANTIATE(32, 24, 256)
+RW_INSTANTIATE(32, 8, 256)

@@ -1,2 +1,2 @@
 #include "rw_inst.cuh"
-RW_INSTANTIATE(4, 24, 256)
+RW_INSTANTIATE(4, 16, 256)

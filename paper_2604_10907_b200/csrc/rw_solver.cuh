@@ -105,12 +105,22 @@ struct Smem {
   static constexpr int TILE = WP * BLK; // rows per tile
   static constexpr int MAXP = L + 1;    // pieces per warp block
   static constexpr int CAP = 4096;      // polish candidates kept in smem
+  static constexpr int RAWW = 64;       // RAW b values a warp can hand the walker per tile
+  // TMA ring: each producer warp streams SR-row stages of its blocks (cp.async.bulk)
+  static constexpr int SR = (MM <= 4) ? 128 : ((MM <= 8) ? 64 : 32);
+  static constexpr int RL = SR / 32;    // rows per lane per stage
+  static constexpr int STAGE_BYTES = SR * MM * 8;
+  static_assert(L % RL == 0, "a block is a whole number of stages");
+  __align__(128) unsigned char ring[WP][2][STAGE_BYTES];
+  unsigned long long stage_bar[WP][2];
+  double raw[2][WP][RAWW];              // RAW sub-segments' b (tile parity)
   Piece pieces[2][WP][MAXP];            // double-buffered by tile parity
   int npieces[2][WP];
+  unsigned long long tot_bar[2], full_bar[2], empty_bar[2];  // mbarriers (tile parity)
   double tot_b[2][WP], tot_a[2][WP];    // per-block approximate sums (sum b, sum |b|)
   union {
     unsigned long long cand[CAP];       // polish candidates
-    double bscr[2][WP][BLK];            // a pass's b values (tile parity), for RAW re-adds
+    double bscr[WP][BLK];               // each warp's b values of its current block
   };
   unsigned hist[256];
   // reduction scratch
@@ -305,16 +315,26 @@ struct Solver {
   // the bit pattern of S and re-adding RAW rows with IEEE adds — the exact bits of the
   // reference's left-to-right sum, overlapped with the next tile's loads.
   static constexpr int WP = SM::WP, BLK = SM::BLK, TILE = SM::TILE, MAXP = SM::MAXP;
-  static constexpr int BAR_TOT = 1, BAR_FULL = 2, BAR_EMPTY = 4;  // named barrier ids
   // Rows per load group (all loads of a group are in flight together).
-  static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : ((MM <= 16) ? 2 : 1));
-  static_assert(L % G == 0, "L must be a multiple of the load group");
 
-  __device__ __forceinline__ static void bar_sync(int id, int cnt) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+  // mbarriers: per-warp waits, so a slow warp only delays the warps that need its data.
+  __device__ __forceinline__ static void mbar_init(unsigned long long* bar, unsigned count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
   }
-  __device__ __forceinline__ static void bar_arrive(int id, int cnt) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+  __device__ __forceinline__ static void mbar_arrive(unsigned long long* bar) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a)
+                 : "memory");
+  }
+  __device__ __forceinline__ static void mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(a),
+        "r"(parity), "r"(0x989680)
+        : "memory");
   }
   // Warp sums evaluated in one fixed order and broadcast, so every lane holds the same bits.
   __device__ __forceinline__ static double warp_sum_d(double x) {
@@ -338,7 +358,7 @@ struct Solver {
     const double y = fabs(b) * scale;
     const double t = y + 0x1p52;
     const long long q = __double_as_longlong(t) - 0x4330000000000000ll;
-    tie = tie || (fabs((t - 0x1p52) - y) == 0.5);
+    tie |= (fabs((t - 0x1p52) - y) == 0.5);
     return (b < 0.0) ? -q : q;
   }
 
@@ -385,13 +405,20 @@ struct Solver {
     if (tid_ == 0) {
       SMX.S = 0.0;
       if (MODE == PASS_EVAL) SMX.eval_passes++;
+      for (int q = 0; q < 2; ++q) {
+        mbar_init(&SMX.tot_bar[q], WP * 32);
+        mbar_init(&SMX.full_bar[q], WP * 32);
+        mbar_init(&SMX.empty_bar[q], 32);
+        for (int w2 = 0; w2 < WP; ++w2) mbar_init(&SMX.stage_bar[w2][q], 1);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (tid_ < MM) SMX.counts[tid_] = 0;
     __syncthreads();
     const int ntiles = (n_ + TILE - 1) / TILE;
     const long long t_pass = clock64();
     if (wid_ == WP) {
-      walk<MODE, FULLM>(ntiles);
+      walk<MODE, FULLM>(ntiles, a, m_, mo_in);
     } else {
       produce<MODE, FULLM, WMO>(n_, ntiles, a, m_, want_counts, mo_out, mo_in);
     }
@@ -399,56 +426,68 @@ struct Solver {
     if (tid_ == 0) SMX.prof[PR_PASS] += clock64() - t_pass;
   }
 
-  // Walker warp: applies the pieces of every tile in row order.  Pieces are fetched 32 at
-  // a time (one per lane) and broadcast; RAW rows are re-added by lane 0 from the tile's
-  // smem copy of b (double-buffered with the pieces), so the walk never touches HBM/L2.
+  // Walker warp: applies the pieces of every tile in row order.  Lane 0 walks the pieces
+  // (SAFE: three integer ops on the bit pattern of S; RAW: IEEE adds of the b values the
+  // producer left in smem); only a RAW piece whose values did not fit the small ring, or
+  // a SAFE piece whose premise fails, needs the whole warp to recompute rows from L2.
   template <int MODE, bool FULLM>
-  __device__ __forceinline__ void walk(int ntiles) {
+  __device__ __forceinline__ void walk(int ntiles, const double (&a)[MM], int m_,
+                                       const uint8_t* mo_in) {
     const int lane_ = threadIdx.x & 31;
-    double S = 0.0;
+    double S = 0.0;  // valid in lane 0
     long long raw_rows = 0;
     for (int k = 0; k < ntiles; ++k) {
       const int s = k & 1;
       const long long t0 = clock64();
-      bar_sync(BAR_FULL + s, T);
+      mbar_wait(&SMX.full_bar[s], (k >> 1) & 1);
       const long long t1 = clock64();
       for (int w2 = 0; w2 < WP; ++w2) {
-        const int np = SMX.npieces[s][w2];
-        const double* scr = SMX.bscr[s][w2];
-        const int blk0 = k * TILE + w2 * BLK;
-        for (int p0 = 0; p0 < np; p0 += 32) {
-          Piece mine;
-          if (p0 + lane_ < np) mine = SMX.pieces[s][w2][p0 + lane_];
-          const int cnt = min(32, np - p0);
-          for (int pp = 0; pp < cnt; ++pp) {
-            const long long q = __shfl_sync(FULL, mine.q, pp);
-            const int row = __shfl_sync(FULL, mine.row, pp);
-            const int nrows = __shfl_sync(FULL, mine.nrows, pp);
-            const int key = __shfl_sync(FULL, mine.key, pp);
-            const int kind = __shfl_sync(FULL, mine.kind, pp);
-            bool done = false;
-            if (kind == PIECE_SAFE) {
-              const long long bits = __double_as_longlong(S);
-              const int ex = (int)((bits >> 52) & 0x7ff) - 1023;
-              const int ng = bits < 0 ? 1 : 0;
-              if (ex == (key >> 1) && ng == (key & 1) && ex > -1000) {
-                S = apply_quanta(S, q, q);
-                done = true;
-              }
-            }
-            if (!done) {  // RAW (or a SAFE piece whose premise failed): exact IEEE adds
-              raw_rows += nrows;
-              if (lane_ == 0) {
-                const double* src = scr + (row - blk0);
+        int np = SMX.npieces[s][w2];
+        int p = 0;
+        while (p < np) {
+          int hard_row = -1, hard_n = 0;  // a piece lane 0 cannot finish alone
+          if (lane_ == 0) {
+            for (; p < np; ++p) {
+              const Piece& pc = SMX.pieces[s][w2][p];
+              const long long q = pc.q;
+              const int kind = pc.kind, nrows = pc.nrows;
+              if (kind == PIECE_SAFE) {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(S);
+                if ((int)(bits >> 52) == pc.key) {  // S is in the piece's binade: add its step
+                  S = __longlong_as_double((long long)(bits + (unsigned long long)q));
+                  continue;
+                }
+              } else if (q >= 0) {
+                const double* src = SMX.raw[s][w2] + q;
+                raw_rows += nrows;
 #pragma unroll 8
                 for (int r = 0; r < nrows; ++r) S = __dadd_rn(S, src[r]);
+                continue;
               }
-              S = __shfl_sync(FULL, S, 0);
+              hard_row = pc.row;
+              hard_n = nrows;
+              ++p;
+              break;
+            }
+          }
+          hard_n = __shfl_sync(FULL, hard_n, 0);
+          p = __shfl_sync(FULL, p, 0);
+          if (hard_n > 0) {  // recompute the rows from the scores, add them in order
+            hard_row = __shfl_sync(FULL, hard_row, 0);
+            raw_rows += hard_n;
+            for (int r0 = 0; r0 < hard_n; r0 += 32) {
+              const int c = min(32, hard_n - r0);
+              const double bj =
+                  (lane_ < c) ? row_b<MODE, FULLM>(hard_row + r0 + lane_, a, m_, mo_in) : 0.0;
+              for (int r = 0; r < c; ++r) {
+                const double x = __shfl_sync(FULL, bj, r);
+                if (lane_ == 0) S = __dadd_rn(S, x);
+              }
             }
           }
         }
       }
-      if (k + 2 < ntiles) bar_arrive(BAR_EMPTY + s, T);
+      mbar_arrive(&SMX.empty_bar[s]);
       if (lane_ == 0) {
         SMX.prof[PR_WALK_WAIT] += t1 - t0;
         SMX.prof[PR_WALK_BUSY] += clock64() - t1;
@@ -461,66 +500,149 @@ struct Solver {
     }
   }
 
-  // A block near a binade crossing (or holding a half-ulp tie): classify each 32-row
-  // sub-segment with its own margin; consecutive SAFE sub-segments of one binade merge.
-  // b comes from this warp's smem scratch.  Returns the number of pieces written.
-  __device__ __noinline__ int slow_block(const double* scr, const int blk0, const int n_,
-                                         double Pg, double Ag, Piece* out) {
+  // A block near a binade crossing (or holding a half-ulp tie): lane g classifies 32-row
+  // sub-segment g with its own margin (sub-segment sums, then one lane scan for the
+  // prefixes); consecutive SAFE sub-segments of one binade merge into one piece.
+  // b comes from this warp's smem copy.  Returns the number of pieces written.
+  __device__ __noinline__ int slow_block(const double* scr, double* raw, const int blk0,
+                                         const int n_, const double Pw, const double Aw,
+                                         Piece* out) {
+    static_assert(L <= 32, "one lane per sub-segment");
     const int lane_ = threadIdx.x & 31;
-    int np = 0;
+    const int nsub = min(L, (n_ - blk0 + 31) / 32);
+    const int row_l = blk0 + lane_ * 32;
+    const int cnt_l = (lane_ < nsub) ? min(32, n_ - row_l) : 0;
+    const double* mine = scr + lane_ * 32;
+    double sb = 0.0, sa = 0.0;
+    if (lane_ < nsub) {
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) {  // rotated: conflict-free banks
+        const double x = mine[(r + lane_) & 31];
+        sb += x;
+        sa += fabs(x);
+      }
+    }
+    double ib = sb, ia = sa;  // inclusive lane scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double tb = __shfl_up_sync(FULL, ib, off), ta = __shfl_up_sync(FULL, ia, off);
+      if (lane_ >= off) {
+        ib += tb;
+        ia += ta;
+      }
+    }
+    double eb = __shfl_up_sync(FULL, ib, 1), ea = __shfl_up_sync(FULL, ia, 1);
+    if (lane_ == 0) eb = ea = 0.0;
+    const double Pl = Pw + eb, Al = Aw + ea;
+    const double E = ((double)row_l + (double)cnt_l + 64.0) * 0x1p-51 * (Al + sa) + sa * 0x1p-48;
+    int e = 0, ng = 0;
+    bool safe = lane_ < nsub &&
+                range_binade(Pl - 0.5 * (sa - sb) - E, Pl + 0.5 * (sa + sb) + E, e, ng);
+    long long Q = 0;
+    if (safe) {
+      const double scale = __longlong_as_double((long long)(52 - e + 1023) << 52);
+      bool tie = false;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) Q += quanta(mine[(r + lane_) & 31], scale, tie);
+      safe = !tie;
+    }
+    const int key = safe ? (2 * e + ng) : 0;
+    int np = 0, raw_used = 0;
     long long Qrun = 0;
     int run_key = 0, run_row = 0, run_rows = 0;
-    auto emit = [&](long long q, int row, int nrows, int key, int kind) {
-      if (lane_ == 0) {
-        Piece& pc = out[np];
-        pc.q = q;
-        pc.row = row;
-        pc.nrows = nrows;
-        pc.key = key;
-        pc.kind = kind;
+    for (int g = 0; g < nsub; ++g) {  // warp-uniform merge in row order
+      const bool sg = __shfl_sync(FULL, safe, g);
+      const int kg = __shfl_sync(FULL, key, g);
+      const long long qg = __shfl_sync(FULL, Q, g);
+      const int cg = __shfl_sync(FULL, cnt_l, g);
+      const int rg = blk0 + g * 32;
+      if (sg && run_rows > 0 && kg == run_key) {
+        Qrun += qg;
+        run_rows += cg;
+        continue;
       }
-      ++np;
-    };
-#pragma unroll 1
-    for (int g = 0; g < L; ++g) {
-      const int row_g = blk0 + g * 32;
-      if (row_g >= n_) break;
-      const int cnt_g = min(32, n_ - row_g);
-      const double bg = scr[g * 32 + lane_];
-      const double sbg = warp_sum_d(bg), sag = warp_sum_d(fabs(bg));
-      const double Eg =
-          ((double)row_g + (double)cnt_g + 64.0) * 0x1p-51 * (Ag + sag) + sag * 0x1p-48;
-      int e = 0, ng = 0;
-      bool safe = range_binade(Pg - 0.5 * (sag - sbg) - Eg, Pg + 0.5 * (sag + sbg) + Eg, e, ng);
-      long long q = 0;
-      if (safe) {
-        bool tie = false;
-        q = quanta(bg, __longlong_as_double((long long)(52 - e + 1023) << 52), tie);
-        safe = !__any_sync(FULL, tie);
+      if (run_rows > 0) {
+        if (lane_ == 0) set_safe(out[np], Qrun, run_row, run_rows, run_key);
+        ++np;
       }
-      const int key = 2 * e + ng;
-      if (safe && run_rows > 0 && key == run_key) {
-        Qrun += q;
-        run_rows += cnt_g;
+      if (sg) {
+        Qrun = qg;
+        run_key = kg;
+        run_row = rg;
+        run_rows = cg;
       } else {
-        if (run_rows > 0) emit(warp_sum_ll(Qrun), run_row, run_rows, run_key, PIECE_SAFE);
-        if (safe) {
-          Qrun = q;
-          run_key = key;
-          run_row = row_g;
-          run_rows = cnt_g;
-        } else {
-          Qrun = 0;
-          run_rows = 0;
-          emit(0, row_g, cnt_g, 0, PIECE_RAW);
+        run_rows = 0;
+        // hand the walker the b values (or -1: it recomputes the rows from the scores)
+        long long off = -1;
+        if (raw_used + cg <= SM::RAWW) {
+          if (lane_ < cg) raw[raw_used + lane_] = scr[g * 32 + lane_];
+          off = raw_used;
+          raw_used += cg;
         }
+        if (lane_ == 0) {
+          Piece& pc = out[np];
+          pc.q = off;
+          pc.row = rg;
+          pc.nrows = cg;
+          pc.key = -1;
+          pc.kind = PIECE_RAW;
+        }
+        ++np;
       }
-      Pg += sbg;
-      Ag += sag;
     }
-    if (run_rows > 0) emit(warp_sum_ll(Qrun), run_row, run_rows, run_key, PIECE_SAFE);
+    if (run_rows > 0) {
+      if (lane_ == 0) set_safe(out[np], Qrun, run_row, run_rows, run_key);
+      ++np;
+    }
     return np;
   }
+
+  // A SAFE piece stores the expected top 12 bits of S (sign | biased exponent) and the
+  // signed step of its bit pattern, so the walker's check-and-apply is three integer ops.
+  __device__ __forceinline__ static void set_safe(Piece& pc, long long q, int row, int nrows,
+                                                  int key) {
+    const int e = key >> 1, ng = key & 1;
+    pc.q = ng ? -q : q;
+    pc.row = row;
+    pc.nrows = nrows;
+    pc.key = (ng << 11) | (e + 1023);
+    pc.kind = PIECE_SAFE;
+  }
+
+  // 1-D TMA: bulk copy global -> this CTA's smem, completion counted on an mbarrier.
+  __device__ __forceinline__ static void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(a),
+                 "r"(bytes)
+                 : "memory");
+  }
+  __device__ __forceinline__ static void tma_load_1d(void* dst, const void* src, unsigned bytes,
+                                                     unsigned long long* bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+  }
+
+  // 256-bit load (sm_100: LDG.E.ENL2.256): a 4-model row in one instruction.  Volatile
+  // on purpose: ptxas never reorders volatile accesses, so a group's loads (issued in
+  // program order before the group's volatile smem stores) stay batched in flight —
+  // with plain loads ptxas sinks each load to its first use and keeps ~1 row in flight.
+  __device__ __forceinline__ static void ld4(const double* p, double& x0, double& x1, double& x2,
+                                             double& x3) {
+    asm volatile("ld.volatile.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(x0), "=d"(x1), "=d"(x2), "=d"(x3)
+                 : "l"(p));
+  }
+  __device__ __forceinline__ static void st_shared_volatile(double* p, double x) {
+    asm volatile("st.volatile.shared.f64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)),
+                 "d"(x));
+  }
+  // Rows per load group (all loads of a group are in flight together).
+  static constexpr int G = (MM <= 4) ? 8 : ((MM <= 8) ? 4 : ((MM <= 16) ? 2 : 1));
+  static_assert(L % G == 0, "L must be a multiple of the load group");
 
   template <int MODE, bool FULLM, bool WMO>
   __device__ __forceinline__ void produce(const int n_, const int ntiles, const double (&a)[MM],
@@ -528,6 +650,9 @@ struct Solver {
                                           const uint8_t* mo_in) {
     const int lane_ = threadIdx.x & 31, wid_ = threadIdx.x >> 5;
     const double* __restrict__ sc = jb.scores;
+    double* scr = SMX.bscr[wid_];
+    // full-width rows: compile-time load shape (the ABI guarantees 32-byte alignment)
+    constexpr bool vec4 = FULLM && (MM % 4 == 0);
     const bool vec2 = FULLM ? (MM % 2 == 0) : ((m_ & 1) == 0);
     double P = 0.0, A = 0.0;  // approximate (sum b, sum |b|) of every row before the tile
     // estimated block total: predicts the binade before the block's prefix is known
@@ -535,14 +660,29 @@ struct Solver {
     unsigned long long pk[NPK];
 #pragma unroll
     for (int q = 0; q < NPK; ++q) pk[q] = 0ull;
+    // TMA streaming (rows of a whole number of 16-byte chunks): lane 0 keeps the next stage
+    // of this warp's row sequence in flight while the warp computes the current one.
+    constexpr int RL = SM::RL, SR = SM::SR, NSTG = L / RL;
+    const bool tma = (m_ & 1) == 0;  // pass-uniform
+    auto stage_row = [&](const int t) { return (t / NSTG) * TILE + wid_ * BLK + (t % NSTG) * SR; };
+    auto issue = [&](const int t) {  // no-op past the last row
+      const int r0 = stage_row(t);
+      if (lane_ == 0 && r0 < n_) {
+        const int nv = min(SR, n_ - r0);
+        const unsigned bytes = (unsigned)(nv * m_ * 8);
+        unsigned long long* bar = &SMX.stage_bar[wid_][t & 1];
+        mbar_expect_tx(bar, bytes);
+        tma_load_1d(SMX.ring[wid_][t & 1], sc + (size_t)r0 * m_, bytes, bar);
+      }
+    };
+    if (tma) issue(0);
     for (int k = 0; k < ntiles; ++k) {
       const int s = k & 1;
       const int blk0 = k * TILE + wid_ * BLK;
       const bool live = blk0 < n_;  // warp-uniform
       const long long te = clock64();
-      if (k >= 2) bar_sync(BAR_EMPTY + s, T);  // the walker is done with tile k-2's slot
+      if (k >= 2) mbar_wait(&SMX.empty_bar[s], ((k - 2) >> 1) & 1);  // walker done with k-2
       if (wid_ == 0 && lane_ == 0) SMX.prof[PR_EMPTY] += clock64() - te;
-      double* scr = SMX.bscr[s][wid_];
       int e_pred = 0, ng_pred = 0;
       const bool pred_ok = in_binade(P + (double)wid_ * blk_est, 0.0, e_pred, ng_pred);
       const double scale =
@@ -552,8 +692,73 @@ struct Solver {
       double sb = 0.0, sa = 0.0;
       const long long t0 = clock64();
       // -- loads + priced argmax + speculative quanta -----------------------------------
-      if (live) {
+      auto row_work = [&](const double* v, const int g, const int j) {
+        const bool valid = j < n_;
+        double bj = 0.0;
+        int arg = 0;
+        if (valid) {
+          if (MODE == PASS_EVAL) {
+            bj = __dsub_rn(v[0], a[0]);
+#pragma unroll
+            for (int i = 1; i < MM; ++i) {
+              if (FULLM || i < m_) {
+                const double x = __dsub_rn(v[i], a[i]);
+                if (x > bj) {
+                  bj = x;
+                  arg = i;
+                }
+              }
+            }
+          } else {
+            arg = mo_in ? (int)mo_in[j] : 0;
+            bj = v[arg];
+          }
+        }
+        scr[g * 32 + lane_] = bj;
+        Q += quanta(bj, scale, tie);
+        sb += bj;
+        sa += fabs(bj);
+        const bool cnt = valid && want_counts;
+        if (NPK == 1) {
+          pk[0] += cnt ? (1ull << (arg * 16)) : 0ull;
+        } else {
+#pragma unroll
+          for (int q = 0; q < NPK; ++q)
+            pk[q] += (cnt && (arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+        }
+        if (WMO && valid) mo_out[j] = (uint8_t)arg;
+      };
+      if (live && tma) {
 #pragma unroll 1
+        for (int st = 0; st < NSTG; ++st) {
+          const int t = k * NSTG + st;
+          if (stage_row(t) >= n_) break;  // never issued: rows past the end stay b = 0
+          issue(t + 1);  // the other slot was released by the __syncwarp below
+          mbar_wait(&SMX.stage_bar[wid_][t & 1], (t >> 1) & 1);
+          const unsigned char* stg = SMX.ring[wid_][t & 1];
+#pragma unroll
+          for (int i = 0; i < RL; ++i) {
+            const int r = i * 32 + lane_;
+            double v[MM];
+            const double2* rp = reinterpret_cast<const double2*>(stg + (size_t)r * m_ * 8);
+#pragma unroll
+            for (int q = 0; q < MM / 2; ++q) {
+              if (FULLM || 2 * q < m_) {
+                const double2 x = rp[q];
+                v[2 * q] = x.x;
+                v[2 * q + 1] = x.y;
+              } else {
+                v[2 * q] = 0.0;
+                v[2 * q + 1] = 0.0;
+              }
+            }
+            if (MM & 1) v[MM - 1] = 0.0;
+            row_work(v, st * RL + i, blk0 + st * SR + r);
+          }
+          __syncwarp();  // every lane is done with this slot before it is refilled
+        }
+      } else if (live) {
+#pragma unroll
         for (int g0 = 0; g0 < L; g0 += G) {
           double v[G][MODE == PASS_EVAL ? MM : 1];
           int ag[G];
@@ -562,7 +767,12 @@ struct Solver {
             const int j = min(blk0 + (g0 + gg) * 32 + lane_, n_ - 1);
             const double* row = sc + (size_t)j * m_;
             if (MODE == PASS_EVAL) {
-              if (vec2) {
+              if constexpr (vec4) {
+#pragma unroll
+                for (int i = 0; i < MM / 4; ++i)
+                  ld4(row + 4 * i, v[gg][4 * i], v[gg][4 * i + 1], v[gg][4 * i + 2],
+                      v[gg][4 * i + 3]);
+              } else if (vec2) {
                 const double2* r2 = reinterpret_cast<const double2*>(row);
 #pragma unroll
                 for (int i = 0; i < MM / 2; ++i) {
@@ -605,24 +815,23 @@ struct Solver {
               bj = v[gg][0];
               arg = ag[gg];
             }
+            // branch-free per row: a branch here would stop ptxas from batching the
+            // next rows' loads ahead of this row's arithmetic
             const bool valid = j < n_;
             bj = valid ? bj : 0.0;
-            scr[(g0 + gg) * 32 + lane_] = bj;
+            st_shared_volatile(&scr[(g0 + gg) * 32 + lane_], bj);
             Q += quanta(bj, scale, tie);
             sb += bj;
             sa += fabs(bj);
-            if (valid) {
-              if (want_counts) {
-                if (NPK == 1) {
-                  pk[0] += 1ull << (arg * 16);
-                } else {
+            const bool cnt = valid && want_counts;
+            if (NPK == 1) {
+              pk[0] += cnt ? (1ull << (arg * 16)) : 0ull;
+            } else {
 #pragma unroll
-                  for (int q = 0; q < NPK; ++q)
-                    pk[q] += ((arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
-                }
-              }
-              if (WMO) mo_out[j] = (uint8_t)arg;
+              for (int q = 0; q < NPK; ++q)
+                pk[q] += (cnt && (arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
             }
+            if (WMO && valid) mo_out[j] = (uint8_t)arg;
           }
         }
       }
@@ -634,7 +843,8 @@ struct Solver {
         SMX.tot_a[s][wid_] = sa;
       }
       const long long t1 = clock64();
-      bar_sync(BAR_TOT, WP * 32);
+      mbar_arrive(&SMX.tot_bar[s]);
+      mbar_wait(&SMX.tot_bar[s], (k >> 1) & 1);
       const long long t2 = clock64();
       double Pw = P, Aw = A;
       const double P_prev = P;
@@ -666,24 +876,18 @@ struct Solver {
             e0 == e_pred && n0 == ng_pred && !__any_sync(FULL, tie);
         if (fast) {  // whole block inside the predicted binade: one integer piece
           Q = warp_sum_ll(Q);
-          if (lane_ == 0) {
-            Piece& pc = out[0];
-            pc.q = Q;
-            pc.row = blk0;
-            pc.nrows = nrows;
-            pc.key = 2 * e0 + n0;
-            pc.kind = PIECE_SAFE;
-          }
+          if (lane_ == 0) set_safe(out[0], Q, blk0, nrows, 2 * e0 + n0);
           np = 1;
           if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_FAST], 1ull);
         } else {  // 32-row sub-segments from the smem copy of b
           __syncwarp();
-          np = slow_block(scr, blk0, n_, Pw, Aw, out);
+          np = slow_block(scr, SMX.raw[s][wid_], blk0, n_, Pw, Aw, out);
           if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_SLOW], 1ull);
         }
       }
       if (lane_ == 0) SMX.npieces[s][wid_] = np;
-      bar_arrive(BAR_FULL + s, T);
+      __syncwarp();
+      mbar_arrive(&SMX.full_bar[s]);
       // per-model counts: 16-bit packed lanes, flushed before they can overflow
       if (want_counts && ((k & 31) == 31 || k == ntiles - 1)) {
 #pragma unroll
