@@ -1,0 +1,70 @@
+"""The drop-in boundary, end to end: the reference's OWN acceptance binary
+(/root/reference/proj/tests/acceptance.cpp, 10 release criteria), relinked by
+integration/Makefile so that solve_dual / assign_prompts / dual_objective /
+optimize_fractions / optimize_beta / select_setup come from integration/
+routeplan_b200_shim.cpp -> librw_b200.so, must pass every criterion on the B200 — and
+its printed numbers must equal the unmodified CPU build's."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+B200 = os.path.join(ROOT, "integration", "_build", "acceptance_b200")
+REF = os.path.join(ROOT, "integration", "_build", "acceptance_ref")
+
+
+_CACHE = {}
+
+
+def _run(exe, timeout=600):
+    if exe in _CACHE:
+        return _CACHE[exe]
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (make -C integration where /root/reference exists)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=timeout)
+    lines = {}
+    for ln in out.stdout.splitlines():
+        m = re.match(r"criterion (\d+): (PASS|FAIL) — (.*)", ln)
+        if m:
+            lines[int(m.group(1))] = (m.group(2), m.group(3))
+    _CACHE[exe] = (out, lines)
+    return out, lines
+
+
+def _numbers_without_timing(detail):
+    # drop wall-clock fields ("0.238 s (budget 60 s)") before comparing the rest
+    detail = re.sub(r"[0-9.e+-]+ s \(budget [0-9.]+ s\)", "", detail)
+    return detail
+
+
+def test_shim_symbols_replace_the_reference():
+    if not os.path.exists(B200):
+        pytest.skip("integration binary not built")
+    syms = subprocess.run(["nm", "-C", B200], capture_output=True, text=True).stdout
+    for fn in ["solve_dual", "optimize_beta", "optimize_fractions", "select_setup",
+               "assign_prompts", "dual_objective"]:
+        assert re.search(rf" T routeplan::{fn}\(", syms), fn
+        assert f"ref_cpu_{fn}" in syms  # the reference definition is renamed out of the way
+    libs = subprocess.run(["ldd", B200], capture_output=True, text=True).stdout
+    assert "librw_b200.so" in libs
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_passes_on_b200():
+    out, got = _run(B200)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert sorted(got) == list(range(1, 11)), out.stdout
+    for k, (verdict, detail) in got.items():
+        assert verdict == "PASS", (k, detail)
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_numbers_match_cpu_build():
+    _, gpu = _run(B200)
+    _, cpu = _run(REF)
+    for k in range(1, 11):
+        if k in (4, 5, 8):  # criteria on functions the shim does not replace
+            continue
+        assert _numbers_without_timing(gpu[k][1]) == _numbers_without_timing(cpu[k][1]), k
