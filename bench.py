@@ -290,19 +290,11 @@ def main():
     local_ms = ev0.elapsed_time(ev1)
     mine = np.concatenate(recs)
     # gather the fixed-size records (one collective) and reduce deterministically
+    from paper_2604_10907_b200 import shard
     if world > 1:
-        t = torch.from_numpy(mine.view(np.uint8).copy()).to(dev)
-        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-        dist.all_gather(sizes, torch.tensor([t.numel()], dtype=torch.int64, device=dev))
-        mx = int(max(x.item() for x in sizes))
-        buf = torch.zeros(mx, dtype=torch.uint8, device=dev)
-        buf[: t.numel()] = t
-        outs = [torch.zeros(mx, dtype=torch.uint8, device=dev) for _ in range(world)]
-        dist.all_gather(outs, buf)
-        allrec = np.concatenate([o[: int(sz.item())].cpu().numpy().view(_abi.RECORD_DTYPE)
-                                 for o, sz in zip(outs, sizes)])
+        allrec = shard.gather_records(mine, device=dev)
         tt = torch.tensor([local_ms, kernel_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # time = max over ranks
         step_ms = float(tt[0].item()) / args.steps
         kern_ms = float(tt[1].item()) / args.steps
     else:
@@ -320,11 +312,8 @@ def main():
     evals_step = passes_total * cfg.n
     value = evals_step / (step_ms / 1e3)
     # winner per SLO (wall time to optimal setup = one step for the whole SLO sweep)
-    winners = {}
-    for t in taus:
-        sel = allrec[allrec["tau_ms"] == t]
-        b = rw.reduce_records(sel)
-        winners[str(float(t))] = int(sel[b]["setup_id"]) if b >= 0 else None
+    winners = {str(t): (int(allrec[i]["setup_id"]) if i >= 0 else None)
+               for t, i in shard.winners_per_slo(allrec, [float(t) for t in taus]).items()}
 
     # roofline of the solver kernel: algorithmic bytes = 8*M per eval
     peak, peak_kind = peak_gbs()
