@@ -1135,17 +1135,45 @@ struct Solver {
       s->gather(ok && key >= lo && key <= hi, key);
     }
   };
-  struct RadixRange {  // histogram of one digit of the keys in [lo, hi] matching the prefix
-    unsigned long long lo, hi, pre;
+  struct RadixRange {  // histogram of one 8-bit digit of the keys in [lo, hi]
+    unsigned long long lo, hi;
     int shift;
     Solver* s;
     __device__ __forceinline__ void operator()(bool ok, double bv) {
       const unsigned long long key = dkey(bv);
-      const bool in = ok && key >= lo && key <= hi &&
-                      (shift == 56 || (key >> (shift + 8)) == pre);
-      s->hist_add(in, (unsigned)((key >> shift) & 0xffull));
+      s->hist_add(ok && key >= lo && key <= hi, (unsigned)((key >> shift) & 0xffull));
     }
   };
+  // Warp 0: the digit bin holding the k-th largest counted key -> SMX.sel_lo (bin),
+  // SMX.sel_k (rank inside the bin), SMX.cand_over (the bin's count).
+  __device__ void pick_bin(int k) {
+    if (wid == 0) {
+      const int top = 255 - 8 * lane;  // lane l covers bins [248 - 8l, 255 - 8l]
+      int local = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) local += (int)SMX.hist[top - q];
+      int incl = local;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += t;
+      }
+      const int excl = incl - local;
+      if (excl < k && k <= incl) {
+        int above = excl;
+        for (int q = 0; q < 8; ++q) {
+          const int h = (int)SMX.hist[top - q];
+          if (above + h >= k) {
+            SMX.sel_lo = (unsigned long long)(top - q);
+            SMX.sel_k = k - above;
+            SMX.cand_over = h;
+            break;
+          }
+          above += h;
+        }
+      }
+    }
+  }
 
   // ---- polish_pass (score_dual.cpp:54-76) on SMX.polished --------------------------------
   // Coordinate i's new price is the k-th largest b_j = s_ji - max_{q != i}(s_jq - a_q),
@@ -1238,23 +1266,42 @@ struct Solver {
           __syncthreads();
           nc = SMX.cand_n;
           select_in_cand(nc, r);
-        } else {  // radix select over recomputed keys of the shell
+        } else {
+          // the shell is too full for smem: narrow it one 8-bit key digit per sweep,
+          // starting at the first digit where its bounds differ, until the digit bucket
+          // holding the r-th key fits — then gather that bucket and select in smem
           miss = 3;
-          if (tid == 0) {
-            SMX.sel_prefix = 0ull;
-            SMX.sel_k = r;
-          }
-          for (int shift = 56; shift >= 0; shift -= 8) {
+          unsigned long long plo = lo, phi = hi;
+          int rk = r, cnt_b = cnt;
+          int shift = (lo == hi) ? 0 : ((63 - __clzll((long long)(lo ^ hi))) / 8) * 8;
+          while (cnt_b > SM::CAP && plo != phi) {
             __syncthreads();
             if (tid < 256) SMX.hist[tid] = 0u;
             __syncthreads();
-            RadixRange rr{lo, hi, (shift == 56) ? 0ull : (SMX.sel_prefix >> (shift + 8)), shift,
-                          this};
+            RadixRange rr{plo, phi, shift, this};
             polish_sweep<FULLM>(i, a, rr);
             __syncthreads();
-            select_digit(shift);
+            pick_bin(rk);
+            __syncthreads();
+            const unsigned long long d = SMX.sel_lo;
+            rk = SMX.sel_k;
+            cnt_b = SMX.cand_over;
+            const unsigned long long base = (shift >= 56) ? 0ull : ((plo >> (shift + 8)) << (shift + 8));
+            const unsigned long long nlo = base | (d << shift);
+            const unsigned long long nhi = nlo | ((shift == 0) ? 0ull : ((1ull << shift) - 1ull));
+            plo = nlo > plo ? nlo : plo;
+            phi = nhi < phi ? nhi : phi;
+            shift -= 8;
+            if (shift < 0) break;
           }
           __syncthreads();
+          if (tid == 0) SMX.cand_n = 0;
+          __syncthreads();
+          GatherRange gr{plo, phi, this};
+          polish_sweep<FULLM>(i, a, gr);
+          __syncthreads();
+          nc = SMX.cand_n;
+          select_in_cand(min(nc, SM::CAP), rk);
         }
       }
       if (tid == 0) {
@@ -1769,7 +1816,8 @@ struct Solver {
       SMX.eval_passes = 0;
       SMX.polish_passes = 0;
       SMX.repair_calls = 0;
-      for (int i = 0; i < MM; ++i) SMX.pol_delta[i] = 1e-3;
+      // density-aware first window: ~50 of N keys per unit of price near the optimum
+      for (int i = 0; i < MM; ++i) SMX.pol_delta[i] = fmax(50.0 / (double)n, 1e-12);
       SMX.mean_b = 0.5;
       for (int i = 0; i < RW_PROF_SLOTS; ++i) SMX.prof[i] = 0;
       for (int i = 0; i < MM; ++i) SMX.zero[i] = 0.0;

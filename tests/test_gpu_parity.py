@@ -212,3 +212,48 @@ def test_sweep_slo_batch_matches_single_slo(eng, oracle):
             assert bits(part[k]["score"]) == bits(ref["score"])
             assert bits(part[k]["latency_ms"]) == bits(ref["latency_ms"])
             assert int(part[k]["eval_passes"]) == ref["eval_passes"]
+
+
+@pytest.mark.parametrize("name,n,limit", [("C3", 20000, 6), ("C5", 20000, 6), ("C4", 6000, 3)])
+def test_sweep_configs_reduced_vs_oracle(eng, oracle, name, n, limit):
+    """Configs C3 (8 models incl. TP), C5 (adversarial ties: quantised scores, duplicated
+    columns, 1-ulp neighbours) and C4 (16 models, nonlinear 12-knot latency) at reduced N:
+    every record bit-exact vs the C restatement, pass counts included."""
+    from oracle import Params, ProfileTable
+    cfg = wl.config(name, n=n)
+    inp = wl.build_inputs(cfg, limit=limit)
+    s = wl.scores_for(cfg)
+    eng.load_scores(s)
+    eng.load_profiles(inp.koff, inp.kx, inp.ky)
+    tau = cfg.taus[0]
+    bp = wl.with_span_epsilon(wl.truncated_params(), tau, 4.0)
+    opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=tau, kappa=cfg.kappa)
+    recs = eng.sweep(inp.profile_index, inp.retained, opt, bp)
+    prof = ProfileTable(inp.koff, inp.kx, inp.ky)
+    p = Params(sub_max_iters=20, pga_max_iters=5, epsilon=bp.epsilon)
+    for k, r in enumerate(recs):
+        ref = oracle.evaluate_setup(s, prof, inp.profile_index[k], cfg.lambda_rps, tau,
+                                    cfg.kappa, p)
+        assert bool(r["feasible"]) == ref["feasible"], k
+        assert bits(r["score"]) == bits(ref["score"]), (k, float(r["score"]), ref["score"])
+        assert bits(r["latency_ms"]) == bits(ref["latency_ms"]), k
+        assert bits(r["beta"]) == bits(ref["beta"]), k
+        assert np.array_equal(bits(r["w"][:cfg.m]), bits(ref["w"])), k
+        assert int(r["eval_passes"]) == ref["eval_passes"], k
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_eval_pass_full_size_vs_oracle(eng, oracle, name):
+    """BASELINE sizes (1M x 8): one priced pass and the final assignment, bit for bit."""
+    cfg = wl.config(name)
+    s = wl.scores_for(cfg)
+    eng.load_scores(s)
+    m = cfg.m
+    c = np.full(m, cfg.n / m)
+    rng = np.random.default_rng(5)
+    for alpha in [np.zeros(m), rng.uniform(-0.05, 0.05, m), np.arange(m) / 16.0]:
+        g = eng.dual_objective(c, alpha)
+        mo, counts = eng.assign_prompts(alpha)
+        g_ref, counts_ref, mo_ref = oracle.eval_dual(s, c, alpha)
+        assert bits(g) == bits(g_ref)
+        assert np.array_equal(counts, counts_ref) and np.array_equal(mo, mo_ref)
