@@ -87,6 +87,7 @@ enum Prof {
   PR_PSELECT = 12,   // polish candidate selection (cycles)
   PR_PASS = 13,      // eval / fixed passes (cycles)
   PR_REPAIR = 14,    // repair_counts (cycles)
+  PR_MOVES = 15,     // repair Phase-1 rounds (one sweep batch each)
 };
 struct Piece {
   long long q;
@@ -1396,6 +1397,229 @@ struct Solver {
     __syncthreads();
   }
 
+  // ---- repair Phase 1 helpers ---------------------------------------------------------
+  static constexpr int P1BUF = SM::CAP / 2;  // (key, j<<8|v) pairs in the candidate buffer
+
+  __device__ __forceinline__ void move_prompt(int j, int v) {  // thread 0
+    const int u = mo[j];
+    mo[j] = (uint8_t)v;
+    SMX.counts[u]--;
+    SMX.counts[v]++;
+    SMX.delta[u]--;
+    SMX.delta[v]++;
+  }
+
+  // Every Phase-1 candidate (j, v) of the current deltas: f(key(loss), j, v).
+  template <class F>
+  __device__ __forceinline__ void phase1_sweep(F& f) {
+    int dl[MM];
+#pragma unroll
+    for (int q = 0; q < MM; ++q) dl[q] = (q < m) ? SMX.delta[q] : 0;
+    for (int j = tid; j < n; j += T) {
+      const int u = mo[j];
+      if (dl[u] <= 0) continue;
+      const double* row = jb.scores + (size_t)j * m;
+      const double su = __ldg(row + u);
+#pragma unroll
+      for (int v = 0; v < MM; ++v) {
+        if (v < m && dl[v] < 0) f(dkey(__dsub_rn(su, __ldg(row + v))), j, v);
+      }
+    }
+  }
+
+  __device__ void phase1_single() {  // one global minimum (:100-117)
+    double bl = CUDART_INF;
+    int bj = -1, bv = -1;
+    struct MinF {
+      double& bl;
+      int &bj, &bv;
+      const Solver* s;
+      __device__ void operator()(unsigned long long key, int j, int v) {
+        const double loss = dkey_inv(key);
+        if (bj < 0 || loss < bl || (loss == bl && (j < bj || (j == bj && v < bv)))) {
+          bl = loss;
+          bj = j;
+          bv = v;
+        }
+      }
+    } f{bl, bj, bv, this};
+    phase1_sweep(f);
+    block_argmin(bl, bj, bv);
+    if (tid == 0 && bj >= 0) move_prompt(bj, bv);
+    __syncthreads();
+  }
+
+  struct P1Hist {  // 8-bit digit histogram of the candidates selected by (pre, shift[, key])
+    unsigned long long pre;
+    int shift;       // >= 0: digit of the key under prefix `pre`; < 0: digit of j (key == pre)
+    unsigned jpre;   // j prefix above the j digit
+    Solver* s;
+    __device__ __forceinline__ void operator()(unsigned long long key, int j, int v) {
+      (void)v;
+      bool in;
+      unsigned d;
+      if (shift >= 0) {
+        in = (shift >= 56) || (key >> (shift + 8)) == (pre >> (shift + 8));
+        d = (unsigned)((key >> shift) & 0xffull);
+      } else {
+        const int js = -shift - 1;  // 24, 16, 8, 0
+        in = key == pre && (js >= 24 || ((unsigned)j >> (js + 8)) == (jpre >> (js + 8)));
+        d = ((unsigned)j >> js) & 0xffu;
+      }
+      s->hist_add(in, d);
+    }
+  };
+  struct P1Gather {  // candidates below the threshold into the sort buffer
+    unsigned long long kcut;  // key < kcut taken
+    unsigned long long ktie;  // and key == ktie with j < jcut (when jcut > 0)
+    unsigned jcut;
+    Solver* s;
+    __device__ __forceinline__ void operator()(unsigned long long key, int j, int v) {
+      const bool in = key < kcut || (jcut > 0 && key == ktie && (unsigned)j < jcut);
+      if (in) {
+        const int pos = atomicAdd(&s->smx().cand_n, 1);
+        if (pos < P1BUF) {
+          s->smx().cand[2 * pos] = key;
+          s->smx().cand[2 * pos + 1] = ((unsigned long long)(unsigned)j << 8) | (unsigned)v;
+        }
+      }
+    }
+  };
+  __device__ __forceinline__ SM& smx() const { return SMX; }
+
+  // Thread 0: ascending bin walk; returns the bin where the running count would pass cap
+  // (256 if every counted candidate fits) and leaves the count below it in SMX.cand_over.
+  __device__ int p1_pick(int cap, int cum0) {
+    int cum = cum0, stop = 256;
+    for (int d = 0; d < 256; ++d) {
+      const int h = (int)SMX.hist[d];
+      if (cum + h > cap) {
+        stop = d;
+        break;
+      }
+      cum += h;
+    }
+    SMX.cand_over = cum;
+    return stop;
+  }
+
+  __device__ void phase1_batch() {
+    // threshold: narrow the loss key one 8-bit digit per sweep while the smallest bin alone
+    // overflows the buffer; at full key depth narrow on j among equal losses
+    unsigned long long pre = 0ull, kcut = ~0ull, ktie = 0ull;
+    unsigned jcut = 0u, jpre = 0u;
+    int shift = 56;
+    bool done = false;
+    while (!done) {
+      __syncthreads();
+      if (tid < 256) SMX.hist[tid] = 0u;
+      __syncthreads();
+      P1Hist h{pre, shift, jpre, this};
+      phase1_sweep(h);
+      __syncthreads();
+      if (tid == 0) {
+        const int stop = p1_pick(P1BUF, 0);
+        const int cum = SMX.cand_over;
+        int next = 0;  // 0: done, 1: descend
+        if (shift >= 0) {
+          if (stop == 256) {           // all candidates under this prefix fit
+            SMX.sel_lo = (shift >= 56) ? ~0ull : (((pre >> (shift + 8)) + 1ull) << (shift + 8));
+          } else if (cum > 0) {        // take the bins below `stop`
+            SMX.sel_lo = ((shift >= 56) ? 0ull : ((pre >> (shift + 8)) << (shift + 8))) |
+                         ((unsigned long long)stop << shift);
+          } else {                     // the first non-empty bin alone overflows: descend
+            SMX.sel_lo = ((shift >= 56) ? 0ull : ((pre >> (shift + 8)) << (shift + 8))) |
+                         ((unsigned long long)stop << shift);
+            next = 1;
+          }
+          SMX.sel_hi = 0ull;  // jcut
+        } else {
+          const int js = -shift - 1;
+          const unsigned base = (js >= 24) ? 0u : ((jpre >> (js + 8)) << (js + 8));
+          if (stop == 256) {
+            SMX.sel_hi = (js >= 24) ? 0xffffffffull : (unsigned long long)(base + (1u << (js + 8)));
+          } else if (cum > 0 || js == 0) {
+            SMX.sel_hi = (unsigned long long)(base | ((unsigned)stop << js)) + (cum > 0 ? 0u : 1u);
+          } else {
+            SMX.sel_hi = (unsigned long long)(base | ((unsigned)stop << js));
+            next = 1;
+          }
+        }
+        SMX.flag = next;
+      }
+      __syncthreads();
+      const int next = SMX.flag;
+      if (shift >= 0) {
+        if (!next) {
+          kcut = SMX.sel_lo;
+          done = true;
+        } else {
+          pre = SMX.sel_lo;
+          shift -= 8;
+          if (shift < 0) {  // one loss value holds more than the buffer: narrow on j
+            kcut = pre;     // strictly smaller losses: none (the bin was the first)
+            ktie = pre;
+            shift = -25;    // j digit 24
+          }
+        }
+      } else {
+        if (!next) {
+          jcut = (unsigned)SMX.sel_hi;
+          done = true;
+        } else {
+          jpre = (unsigned)SMX.sel_hi;
+          shift += 8;  // -25 -> -17 -> -9 -> -1
+        }
+      }
+    }
+    // gather, sort ascending by (loss key, j, v), apply in order while eligible
+    __syncthreads();
+    if (tid == 0) SMX.cand_n = 0;
+    __syncthreads();
+    P1Gather gth{kcut, ktie, jcut, this};
+    phase1_sweep(gth);
+    __syncthreads();
+    const int nb = min(SMX.cand_n, P1BUF);
+    int np2 = 1;
+    while (np2 < nb) np2 <<= 1;
+    for (int q = nb + tid; q < np2; q += T) {
+      SMX.cand[2 * q] = ~0ull;
+      SMX.cand[2 * q + 1] = ~0ull;
+    }
+    for (int k2 = 2; k2 <= np2; k2 <<= 1) {  // bitonic sort of (key, j<<8|v) pairs
+      for (int jj = k2 >> 1; jj > 0; jj >>= 1) {
+        __syncthreads();
+        for (int q = tid; q < np2; q += T) {
+          const int p = q ^ jj;
+          if (p > q) {
+            const unsigned long long a0 = SMX.cand[2 * q], a1 = SMX.cand[2 * q + 1];
+            const unsigned long long b0 = SMX.cand[2 * p], b1 = SMX.cand[2 * p + 1];
+            const bool gt = (a0 > b0) || (a0 == b0 && a1 > b1);
+            const bool up = (q & k2) == 0;
+            if (gt == up) {
+              SMX.cand[2 * q] = b0;
+              SMX.cand[2 * q + 1] = b1;
+              SMX.cand[2 * p] = a0;
+              SMX.cand[2 * p + 1] = a1;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 0; q < nb; ++q) {
+        bool any = false;
+        for (int i = 0; i < m; ++i) any = any || SMX.delta[i] > 0;
+        if (!any) break;
+        const unsigned long long e = SMX.cand[2 * q + 1];
+        const int j = (int)(e >> 8), v = (int)(e & 0xffull);
+        if (SMX.delta[mo[j]] > 0 && SMX.delta[v] < 0) move_prompt(j, v);
+      }
+    }
+    __syncthreads();
+  }
+
   // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
     const long long t_rep = clock64();
@@ -1404,38 +1628,22 @@ struct Solver {
       for (int i = 0; i < m; ++i) SMX.delta[i] = SMX.counts[i] - SMX.target[i];
     }
     __syncthreads();
-    // Phase 1: min-loss single moves while any surplus remains (:96-118)
+    // Phase 1: min-loss single moves while any surplus remains (:96-118).  Moved prompts
+    // never move again and the surplus / deficit sets only shrink, so the reference's
+    // sequence of global minima of (loss, j, v) can be taken in batches: pick a key
+    // threshold under which at most P1BUF candidates lie, gather and sort them, and apply
+    // them in order while they stay eligible — candidates above the threshold cannot
+    // precede any of them.  A couple of sweeps per batch instead of one per move.
     for (;;) {
-      bool over = false;
-      for (int i = 0; i < m; ++i) over = over || SMX.delta[i] > 0;
-      if (!over) break;
-      double bl = CUDART_INF;
-      int bj = -1, bv = -1;
-      for (int j = tid; j < n; j += T) {
-        int u = mo[j];
-        if (SMX.delta[u] <= 0) continue;
-        const double* row = jb.scores + (size_t)j * m;
-        double su = __ldg(row + u);
-        for (int v = 0; v < m; ++v) {
-          if (SMX.delta[v] >= 0) continue;
-          double loss = __dsub_rn(su, __ldg(row + v));
-          if (bj < 0 || loss < bl) {
-            bl = loss;
-            bj = j;
-            bv = v;
-          }
-        }
+      int surplus = 0;
+      for (int i = 0; i < m; ++i) surplus += SMX.delta[i] > 0 ? SMX.delta[i] : 0;
+      if (surplus == 0) break;
+      if (surplus <= 2) {
+        phase1_single();
+      } else {
+        phase1_batch();
       }
-      block_argmin(bl, bj, bv);
-      if (tid == 0) {
-        int u = mo[bj];
-        mo[bj] = (uint8_t)bv;
-        SMX.counts[u]--;
-        SMX.counts[bv]++;
-        SMX.delta[u]--;
-        SMX.delta[bv]++;
-      }
-      __syncthreads();
+      if (tid == 0) SMX.prof[PR_MOVES] += 1;
     }
     // Phase 2: profitable 2- and 3-cycles (:120-180)
     if (m >= 2) {
