@@ -61,27 +61,48 @@ def schedule_params(rw, wl, name, tau):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region, in-process through
+    NVML (nvidia_ml_py) — a per-sample nvidia-smi subprocess measurably disturbs the
+    run; nvidia-smi is the fallback when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event-reason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+    BITS = [0x8, 0x40, 0x20, 0x4]
 
-    def __init__(self, index):
-        self.index, self.samples, self.stop = index, [], threading.Event()
+    def __init__(self, index, period=0.25):
+        self.index, self.period, self.samples, self.stop = index, period, [], threading.Event()
         self.t = threading.Thread(target=self.run, daemon=True)
+        self.nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+        except Exception:
+            self.nvml = None
+
+    def sample(self):
+        if self.nvml is not None:
+            nv, h = self.nvml
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            return [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip()
+        return [x.strip() for x in out.split(",")] if out else None
 
     def run(self):
         while not self.stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
-                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                smp = self.sample()
+                if smp:
+                    self.samples.append(smp)
             except Exception:
                 pass
-            self.stop.wait(0.2)
+            self.stop.wait(self.period)
 
     def __enter__(self):
         self.t.start()
@@ -101,7 +122,7 @@ class ClockSampler:
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 def peak_gbs():
