@@ -1620,6 +1620,83 @@ struct Solver {
     __syncthreads();
   }
 
+  // Phase 2 gains (:127-141): gain[u][v] = max over prompts j in u of s_jv - s_ju, the
+  // first such j as witness.  One sweep: warp w owns model u = w / wpu (wpu warps per
+  // model split the rows), keeps per-lane maxima for every v, reduces them with shuffles
+  // (gain desc, j asc) and thread 0 merges the parts — no block-wide argmax per (u, v).
+  __device__ void phase2_gains() {
+    const int wpu = (m <= W) ? W / m : 1;  // warps per model
+    const int ub = W / wpu;                // models per batch
+    double* pg = reinterpret_cast<double*>(SMX.cand);   // [W][MM] per-warp partial gains
+    int* pj = reinterpret_cast<int*>(SMX.cand + W * MM);  // [W][MM] witnesses
+    for (int u0 = 0; u0 < m; u0 += ub) {
+      const int u = u0 + wid / wpu, part = wid % wpu;
+      double bg[MM];
+      int bjv[MM];
+#pragma unroll
+      for (int v = 0; v < MM; ++v) {
+        bg[v] = -CUDART_INF;
+        bjv[v] = -1;
+      }
+      if (u < m) {
+        for (int j = part * 32 + lane; j < n; j += wpu * 32) {
+          if (mo[j] != u) continue;
+          const double* row = jb.scores + (size_t)j * m;
+          const double su = __ldg(row + u);
+#pragma unroll
+          for (int v = 0; v < MM; ++v) {
+            if (v < m && v != u) {
+              const double g = __dsub_rn(__ldg(row + v), su);
+              if (bjv[v] < 0 || g > bg[v]) {
+                bg[v] = g;
+                bjv[v] = j;
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < MM; ++v) {  // warp argmax: larger gain, then smaller j
+        double g = bg[v];
+        int j = bjv[v];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double og = __shfl_down_sync(FULL, g, off);
+          const int oj = __shfl_down_sync(FULL, j, off);
+          if (oj >= 0 && (j < 0 || og > g || (og == g && oj < j))) {
+            g = og;
+            j = oj;
+          }
+        }
+        if (lane == 0) {
+          pg[wid * MM + v] = g;
+          pj[wid * MM + v] = j;
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int uu = u0; uu < min(m, u0 + ub); ++uu) {
+          const int w0 = (uu - u0) * wpu;
+          for (int v = 0; v < m; ++v) {
+            double g = -CUDART_INF;
+            int j = -1;
+            for (int p = 0; p < wpu; ++p) {
+              const double og = pg[(w0 + p) * MM + v];
+              const int oj = pj[(w0 + p) * MM + v];
+              if (oj >= 0 && (j < 0 || og > g || (og == g && oj < j))) {
+                g = og;
+                j = oj;
+              }
+            }
+            SMX.gain[uu * m + v] = (j >= 0) ? g : -CUDART_INF;
+            SMX.witness[uu * m + v] = j;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
   // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
     const long long t_rep = clock64();
@@ -1648,39 +1725,7 @@ struct Solver {
     // Phase 2: profitable 2- and 3-cycles (:120-180)
     if (m >= 2) {
       for (int pass_i = 0; pass_i < 10000; ++pass_i) {
-        for (int u = 0; u < m; ++u) {
-          double bg[MM];
-          int bjv[MM];
-#pragma unroll
-          for (int v = 0; v < MM; ++v) {
-            bg[v] = -CUDART_INF;
-            bjv[v] = -1;
-          }
-          for (int j = tid; j < n; j += T) {
-            if (mo[j] != u) continue;
-            const double* row = jb.scores + (size_t)j * m;
-            double su = __ldg(row + u);
-#pragma unroll
-            for (int v = 0; v < MM; ++v) {
-              if (v < m && v != u) {
-                double g = __dsub_rn(__ldg(row + v), su);
-                if (bjv[v] < 0 || g > bg[v]) {
-                  bg[v] = g;
-                  bjv[v] = j;
-                }
-              }
-            }
-          }
-          for (int v = 0; v < m; ++v) {
-            double g = bg[v];
-            int j = bjv[v];
-            block_argmax(g, j);
-            if (tid == 0) {
-              SMX.gain[u * m + v] = (j >= 0) ? g : -CUDART_INF;
-              SMX.witness[u * m + v] = j;
-            }
-          }
-        }
+        phase2_gains();
         __syncthreads();
         if (tid == 0) {
           double best = 1e-15;
