@@ -88,6 +88,8 @@ enum Prof {
   PR_PASS = 13,      // eval / fixed passes (cycles)
   PR_REPAIR = 14,    // repair_counts (cycles)
   PR_MOVES = 15,     // repair Phase-1 rounds (one sweep batch each)
+  PR_P2PASSES = 16,  // repair Phase-2 passes
+  PR_P1MOVED = 17,   // prompts moved by repair Phase 1
 };
 struct Piece {
   long long q;
@@ -1401,6 +1403,7 @@ struct Solver {
   static constexpr int P1BUF = SM::CAP / 2;  // (key, j<<8|v) pairs in the candidate buffer
 
   __device__ __forceinline__ void move_prompt(int j, int v) {  // thread 0
+    SMX.prof[PR_P1MOVED]++;
     const int u = mo[j];
     mo[j] = (uint8_t)v;
     SMX.counts[u]--;
@@ -1725,6 +1728,7 @@ struct Solver {
     // Phase 2: profitable 2- and 3-cycles (:120-180)
     if (m >= 2) {
       for (int pass_i = 0; pass_i < 10000; ++pass_i) {
+        if (tid == 0) SMX.prof[PR_P2PASSES]++;
         phase2_gains();
         __syncthreads();
         if (tid == 0) {
