@@ -409,9 +409,11 @@ struct Solver {
       SMX.S = 0.0;
       if (MODE == PASS_EVAL) SMX.eval_passes++;
       for (int q = 0; q < 2; ++q) {
-        mbar_init(&SMX.tot_bar[q], WP * 32);
-        mbar_init(&SMX.full_bar[q], WP * 32);
-        mbar_init(&SMX.empty_bar[q], 32);
+        // one arrival per warp (lane 0 after __syncwarp + fence): 32x fewer barrier
+        // events than per-lane arrivals, so sleeping waiters are woken far less often
+        mbar_init(&SMX.tot_bar[q], WP);
+        mbar_init(&SMX.full_bar[q], WP);
+        mbar_init(&SMX.empty_bar[q], 1);
         for (int w2 = 0; w2 < WP; ++w2) mbar_init(&SMX.stage_bar[w2][q], 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -490,7 +492,11 @@ struct Solver {
           }
         }
       }
-      mbar_arrive(&SMX.empty_bar[s]);
+      __syncwarp();
+      if (lane_ == 0) {
+        __threadfence_block();
+        mbar_arrive(&SMX.empty_bar[s]);
+      }
       if (lane_ == 0) {
         SMX.prof[PR_WALK_WAIT] += t1 - t0;
         SMX.prof[PR_WALK_BUSY] += clock64() - t1;
@@ -846,7 +852,7 @@ struct Solver {
         SMX.tot_a[s][wid_] = sa;
       }
       const long long t1 = clock64();
-      mbar_arrive(&SMX.tot_bar[s]);
+      if (lane_ == 0) mbar_arrive(&SMX.tot_bar[s]);  // lane 0 wrote the totals
       mbar_wait(&SMX.tot_bar[s], (k >> 1) & 1);
       const long long t2 = clock64();
       double Pw = P, Aw = A;
@@ -890,7 +896,10 @@ struct Solver {
       }
       if (lane_ == 0) SMX.npieces[s][wid_] = np;
       __syncwarp();
-      mbar_arrive(&SMX.full_bar[s]);
+      if (lane_ == 0) {
+        __threadfence_block();  // the warp's pieces / raw values before the release
+        mbar_arrive(&SMX.full_bar[s]);
+      }
       // per-model counts: 16-bit packed lanes, flushed before they can overflow
       if (want_counts && ((k & 31) == 31 || k == ntiles - 1)) {
 #pragma unroll
