@@ -322,6 +322,48 @@ def main():
         allrec = mine
         step_ms = local_ms / args.steps
         kern_ms = kernel_ms / args.steps
+    # end to end through the C-ABI with host buffers: every step H2D-copies the matrix and
+    # tables from pinned memory, sweeps this rank's shard, D2H-reads the records and (N>1)
+    # all-gathers them for the reduction; time = max over ranks
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(s_host).pin_memory().numpy()
+        eng2 = rw.Engine(local)
+        h2d = pinned.nbytes + inp.koff.nbytes + inp.kx.nbytes + inp.ky.nbytes + \
+            inp.profile_index.nbytes + inp.retained.nbytes + taus.nbytes
+        d2h = 0
+        tsum = 0.0
+        passes_e2e = 0
+        iters = max(1, min(args.steps, 3))
+        for it in range(iters + 1):
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            eng2.load_scores(pinned)
+            eng2.load_profiles(inp.koff, inp.kx, inp.ky)
+            recs = []
+            for tg, pg in groups():
+                recs.append(eng2.sweep_slo(inp.profile_index, inp.retained, tg, opt, pg,
+                                           rank, world))
+            r = np.concatenate(recs)
+            d2h = r.nbytes
+            if world > 1:
+                r = shard.gather_records(r, device=dev)
+            shard.winners_per_slo(r, [float(t) for t in taus])
+            dt = time.perf_counter() - t0
+            if it > 0:  # first iteration is warm-up (allocations)
+                tsum += dt
+                passes_e2e = int(r["eval_passes"].sum())
+        if world > 1:
+            tt = torch.tensor([tsum], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tsum = float(tt[0].item())
+        e2e = {"value": passes_e2e * cfg.n / (tsum / iters), "unit": "evals/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": tsum / iters * 1e3}
+        eng2.close()
+
     passes_total = int(allrec["eval_passes"].sum())
     if rank != 0:
         if world > 1:
@@ -347,34 +389,6 @@ def main():
             traffic = tr.get("dram_bytes_per_launch")
     except Exception:
         pass
-
-    # end to end through the C-ABI with host buffers (H2D of the matrix + tables, D2H records)
-    e2e = None
-    if not args.no_e2e:
-        pinned = torch.from_numpy(s_host).pin_memory().numpy()
-        eng2 = rw.Engine(local)
-        h2d = pinned.nbytes + inp.koff.nbytes + inp.kx.nbytes + inp.ky.nbytes + \
-            inp.profile_index.nbytes + inp.retained.nbytes + taus.nbytes
-        d2h = 0
-        tsum = 0.0
-        for it in range(max(1, min(args.steps, 3)) + 1):
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            eng2.load_scores(pinned)
-            eng2.load_profiles(inp.koff, inp.kx, inp.ky)
-            recs = []
-            for tg, pg in groups():
-                recs.append(eng2.sweep_slo(inp.profile_index, inp.retained, tg, opt, pg))
-            r = np.concatenate(recs)
-            dt = time.perf_counter() - t0
-            if it > 0:  # first iteration is warm-up (allocations)
-                tsum += dt
-                d2h = r.nbytes
-        iters = max(1, min(args.steps, 3))
-        e2e = {"value": int(r["eval_passes"].sum()) * cfg.n / (tsum / iters), "unit": "evals/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": tsum / iters * 1e3}
-        eng2.close()
 
     cpu = None
     if not args.no_cpu and world == 1:

@@ -852,8 +852,9 @@ struct Solver {
         SMX.tot_a[s][wid_] = sa;
       }
       const long long t1 = clock64();
-      if (lane_ == 0) mbar_arrive(&SMX.tot_bar[s]);  // lane 0 wrote the totals
-      mbar_wait(&SMX.tot_bar[s], (k >> 1) & 1);
+      // all producer warps' totals: a hardware named barrier (waiting warps are parked, not
+      // polling an mbarrier and stealing issue slots from the warps still streaming)
+      asm volatile("bar.sync 1, %0;" ::"r"(WP * 32) : "memory");
       const long long t2 = clock64();
       double Pw = P, Aw = A;
       const double P_prev = P;
