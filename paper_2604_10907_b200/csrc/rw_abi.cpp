@@ -29,7 +29,6 @@ struct rw_ctx {
   std::vector<int64_t> h_koff;
   // workspace
   uint8_t* d_mo = nullptr;
-  uint64_t* d_keys = nullptr;
   size_t ws_entries = 0;  // slots * n capacity
   // generic io
   void* d_io = nullptr;
@@ -89,12 +88,9 @@ int ensure_ws(rw_ctx* ctx, int slots) {
   size_t need = (size_t)slots * (size_t)ctx->n;
   if (ctx->ws_entries >= need && ctx->d_mo) return RW_OK;
   if (ctx->d_mo) cudaFree(ctx->d_mo);
-  if (ctx->d_keys) cudaFree(ctx->d_keys);
   ctx->d_mo = nullptr;
-  ctx->d_keys = nullptr;
   ctx->ws_entries = 0;
   CK(cudaMalloc(&ctx->d_mo, std::max<size_t>(need, 1)));
-  CK(cudaMalloc(&ctx->d_keys, std::max<size_t>(need, 1) * sizeof(uint64_t)));
   ctx->ws_entries = need;
   return RW_OK;
 }
@@ -145,7 +141,6 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
   j.ky = ctx->d_ky;
   j.shard_count = 1;
   j.ws_model_of = ctx->d_mo;
-  j.ws_keys = ctx->d_keys;
   j.queue = ctx->d_queue;
   j.status_out = ctx->d_status;
   j.prof_out = ctx->d_prof;
@@ -155,7 +150,6 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
 // Launch + time + wait; maps device status to an error.
 int run(rw_ctx* ctx, rw::Job& j, int grid) {
   j.ws_model_of = ctx->d_mo;
-  j.ws_keys = ctx->d_keys;
   CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(unsigned long long), ctx->stream));
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -220,7 +214,6 @@ void rw_destroy(rw_ctx* ctx) {
   cudaFree(ctx->d_kx);
   cudaFree(ctx->d_ky);
   cudaFree(ctx->d_mo);
-  cudaFree(ctx->d_keys);
   cudaFree(ctx->d_io);
   cudaFree(ctx->d_queue);
   cudaFree(ctx->d_status);

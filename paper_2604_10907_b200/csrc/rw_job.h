@@ -54,7 +54,6 @@ struct Job {
   char* msg_out;        // job-level message buffer (256 bytes)
   // workspace, one slot of n entries per CTA
   uint8_t* ws_model_of;
-  uint64_t* ws_keys;
   unsigned long long* queue;
   long long* prof_out;  // optional diagnostics counters [RW_PROF_SLOTS]
 };

@@ -283,12 +283,11 @@ struct Solver {
   const int n, m;
   const int tid, lane, wid;
   uint8_t* mo;               // this CTA's model_of workspace [n]
-  unsigned long long* keys;  // this CTA's radix-select workspace [n]
   const int32_t* pidx;       // current setup's profile indices [m]
 
-  __device__ Solver(const Job& j, uint8_t* mo_, unsigned long long* keys_)
+  __device__ Solver(const Job& j, uint8_t* mo_)
       : jb(j), n(j.n), m(j.m), tid(threadIdx.x), lane(threadIdx.x & 31),
-        wid(threadIdx.x >> 5), mo(mo_), keys(keys_), pidx(nullptr) {}
+        wid(threadIdx.x >> 5), mo(mo_), pidx(nullptr) {}
 
   
   __device__ void fail(int code) {
@@ -2146,8 +2145,7 @@ __global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kern
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int slot = blockIdx.x;
   uint8_t* mo = jb.ws_model_of + (size_t)slot * jb.n;
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(jb.ws_keys) + (size_t)slot * jb.n;
-  Solver<MM, L, T> s(jb, mo, keys);
+  Solver<MM, L, T> s(jb, mo);
   const int tid = threadIdx.x;
   const int m = jb.m, n = jb.n;
 

@@ -242,9 +242,10 @@ def test_sweep_configs_reduced_vs_oracle(eng, oracle, name, n, limit):
         assert int(r["eval_passes"]) == ref["eval_passes"], k
 
 
-@pytest.mark.parametrize("name", ["C3", "C5"])
+@pytest.mark.parametrize("name", ["C3", "C5", "C4"])
 def test_eval_pass_full_size_vs_oracle(eng, oracle, name):
-    """BASELINE sizes (1M x 8): one priced pass and the final assignment, bit for bit."""
+    """BASELINE sizes (1M x 8, 10M x 16): one priced pass and the final assignment, bit
+    for bit."""
     cfg = wl.config(name)
     s = wl.scores_for(cfg)
     eng.load_scores(s)
