@@ -1,2 +1,5 @@
 #include "rw_inst.cuh"
-RW_INSTANTIATE(4, 16, 256)
+#ifndef RW_L4
+#define RW_L4 16  // rows per warp block / 32 (experiments: -DRW_L4=8, 32)
+#endif
+RW_INSTANTIATE(4, RW_L4, 256)

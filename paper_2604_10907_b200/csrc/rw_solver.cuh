@@ -110,16 +110,19 @@ struct Smem {
   static constexpr int CAP = 4096;      // polish candidates kept in smem
   static constexpr int RAWW = 64;       // RAW b values a warp can hand the walker per tile
   // TMA ring: each producer warp streams SR-row stages of its blocks (cp.async.bulk)
-  static constexpr int SR = (MM <= 4) ? 128 : ((MM <= 8) ? 64 : 32);
+#ifndef RW_SR4
+#define RW_SR4 128
+#endif
+  static constexpr int SR = (MM <= 4) ? RW_SR4 : ((MM <= 8) ? 64 : 32);
   static constexpr int RL = SR / 32;    // rows per lane per stage
   static constexpr int STAGE_BYTES = SR * MM * 8;
   static_assert(L % RL == 0, "a block is a whole number of stages");
   __align__(128) unsigned char ring[WP][2][STAGE_BYTES];
   unsigned long long stage_bar[WP][2];
+  unsigned long long full_bar[2], empty_bar[2];
   double raw[2][WP][RAWW];              // RAW sub-segments' b (tile parity)
   Piece pieces[2][WP][MAXP];            // double-buffered by tile parity
   int npieces[2][WP];
-  unsigned long long tot_bar[2], full_bar[2], empty_bar[2];  // mbarriers (tile parity)
   double tot_b[2][WP], tot_a[2][WP];    // per-block approximate sums (sum b, sum |b|)
   union {
     unsigned long long cand[CAP];       // polish candidates
@@ -313,7 +316,7 @@ struct Solver {
   // the block stays in one binade, and publishes a single SAFE piece (e, Q); blocks near a
   // binade crossing (or holding a tie, or with S ~ 0) are split into 32-row sub-segments,
   // each SAFE or RAW.  A dedicated walker warp consumes the pieces in row order
-  // (double-buffered smem ring, named barriers), applying SAFE pieces as integer adds on
+  // (double-buffered smem ring, mbarriers), applying SAFE pieces as integer adds on
   // the bit pattern of S and re-adding RAW rows with IEEE adds — the exact bits of the
   // reference's left-to-right sum, overlapped with the next tile's loads.
   static constexpr int WP = SM::WP, BLK = SM::BLK, TILE = SM::TILE, MAXP = SM::MAXP;
@@ -408,9 +411,6 @@ struct Solver {
       SMX.S = 0.0;
       if (MODE == PASS_EVAL) SMX.eval_passes++;
       for (int q = 0; q < 2; ++q) {
-        // one arrival per warp (lane 0 after __syncwarp + fence): 32x fewer barrier
-        // events than per-lane arrivals, so sleeping waiters are woken far less often
-        mbar_init(&SMX.tot_bar[q], WP);
         mbar_init(&SMX.full_bar[q], WP);
         mbar_init(&SMX.empty_bar[q], 1);
         for (int w2 = 0; w2 < WP; ++w2) mbar_init(&SMX.stage_bar[w2][q], 1);
@@ -512,23 +512,32 @@ struct Solver {
   // sub-segment g with its own margin (sub-segment sums, then one lane scan for the
   // prefixes); consecutive SAFE sub-segments of one binade merge into one piece.
   // b comes from this warp's smem copy.  Returns the number of pieces written.
+  // Everything is lane-parallel (a serial per-sub-segment merge of dependent shuffles and
+  // branches sat on the critical path of every tile holding a slow block): pieces are
+  // numbered by a ballot prefix, SAFE runs summed by a segmented scan, RAW offsets by a
+  // prefix scan of the row counts.
   __device__ __noinline__ int slow_block(const double* scr, double* raw, const int blk0,
                                          const int n_, const double Pw, const double Aw,
                                          Piece* out) {
     static_assert(L <= 32, "one lane per sub-segment");
     const int lane_ = threadIdx.x & 31;
     const int nsub = min(L, (n_ - blk0 + 31) / 32);
+    const bool act = lane_ < nsub;
     const int row_l = blk0 + lane_ * 32;
-    const int cnt_l = (lane_ < nsub) ? min(32, n_ - row_l) : 0;
+    const int cnt_l = act ? min(32, n_ - row_l) : 0;
     const double* mine = scr + lane_ * 32;
+    // approximate sums (any order: the margin E covers every summation order)
     double sb = 0.0, sa = 0.0;
-    if (lane_ < nsub) {
-#pragma unroll 8
+    if (act) {
+      double b4[4] = {0.0, 0.0, 0.0, 0.0}, a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
       for (int r = 0; r < 32; ++r) {  // rotated: conflict-free banks
         const double x = mine[(r + lane_) & 31];
-        sb += x;
-        sa += fabs(x);
+        b4[r & 3] += x;
+        a4[r & 3] += fabs(x);
       }
+      sb = (b4[0] + b4[1]) + (b4[2] + b4[3]);
+      sa = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     }
     double ib = sb, ia = sa;  // inclusive lane scan
 #pragma unroll
@@ -544,8 +553,7 @@ struct Solver {
     const double Pl = Pw + eb, Al = Aw + ea;
     const double E = ((double)row_l + (double)cnt_l + 64.0) * 0x1p-51 * (Al + sa) + sa * 0x1p-48;
     int e = 0, ng = 0;
-    bool safe = lane_ < nsub &&
-                range_binade(Pl - 0.5 * (sa - sb) - E, Pl + 0.5 * (sa + sb) + E, e, ng);
+    bool safe = act && range_binade(Pl - 0.5 * (sa - sb) - E, Pl + 0.5 * (sa + sb) + E, e, ng);
     long long Q = 0;
     if (safe) {
       const double scale = __longlong_as_double((long long)(52 - e + 1023) << 52);
@@ -554,55 +562,54 @@ struct Solver {
       for (int r = 0; r < 32; ++r) Q += quanta(mine[(r + lane_) & 31], scale, tie);
       safe = !tie;
     }
-    const int key = safe ? (2 * e + ng) : 0;
-    int np = 0, raw_used = 0;
-    long long Qrun = 0;
-    int run_key = 0, run_row = 0, run_rows = 0;
-    for (int g = 0; g < nsub; ++g) {  // warp-uniform merge in row order
-      const bool sg = __shfl_sync(FULL, safe, g);
-      const int kg = __shfl_sync(FULL, key, g);
-      const long long qg = __shfl_sync(FULL, Q, g);
-      const int cg = __shfl_sync(FULL, cnt_l, g);
-      const int rg = blk0 + g * 32;
-      if (sg && run_rows > 0 && kg == run_key) {
-        Qrun += qg;
-        run_rows += cg;
-        continue;
-      }
-      if (run_rows > 0) {
-        if (lane_ == 0) set_safe(out[np], Qrun, run_row, run_rows, run_key);
-        ++np;
-      }
-      if (sg) {
-        Qrun = qg;
-        run_key = kg;
-        run_row = rg;
-        run_rows = cg;
-      } else {
-        run_rows = 0;
-        // hand the walker the b values (or -1: it recomputes the rows from the scores)
-        long long off = -1;
-        if (raw_used + cg <= SM::RAWW) {
-          if (lane_ < cg) raw[raw_used + lane_] = scr[g * 32 + lane_];
-          off = raw_used;
-          raw_used += cg;
-        }
-        if (lane_ == 0) {
-          Piece& pc = out[np];
-          pc.q = off;
-          pc.row = rg;
-          pc.nrows = cg;
-          pc.key = -1;
-          pc.kind = PIECE_RAW;
-        }
-        ++np;
+    const int key = 2 * e + ng;  // may be negative (binades below 1)
+    // a SAFE sub-segment continues the previous lane's run when that one is SAFE in the
+    // same binade; every other active lane heads a piece
+    const int key_prev = __shfl_up_sync(FULL, key, 1);
+    const bool safe_prev = __shfl_up_sync(FULL, safe, 1);
+    const bool cont = safe && lane_ > 0 && safe_prev && key_prev == key;
+    const unsigned heads = __ballot_sync(FULL, act && !cont);
+    const int pidx = __popc(heads & ((2u << lane_) - 1u)) - 1;
+    // segmented inclusive scan of (Q, rows) over SAFE runs
+    long long qs = Q;
+    int cs = cnt_l;
+    bool f = !cont;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long tq = __shfl_up_sync(FULL, qs, off);
+      const int tc = __shfl_up_sync(FULL, cs, off);
+      const bool tf = __shfl_up_sync(FULL, f, off);
+      if (lane_ >= off && !f) {
+        qs += tq;
+        cs += tc;
+        f = tf;
       }
     }
-    if (run_rows > 0) {
-      if (lane_ == 0) set_safe(out[np], Qrun, run_row, run_rows, run_key);
-      ++np;
+    const bool next_cont = __shfl_down_sync(FULL, cont, 1) && lane_ + 1 < nsub;
+    // RAW offsets: exclusive prefix of the RAW rows in row order
+    const int rc = (act && !safe) ? cnt_l : 0;
+    int ri = rc;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(FULL, ri, off);
+      if (lane_ >= off) ri += t;
     }
-    return np;
+    const int roff = ri - rc;
+    if (act && safe && !next_cont) {  // end of a SAFE run: one piece for the whole run
+      set_safe(out[pidx], qs, row_l + cnt_l - cs, cs, key);
+    } else if (act && !safe) {
+      // hand the walker the b values (or -1: it recomputes the rows from the scores)
+      const bool fits = roff + cnt_l <= SM::RAWW;
+      if (fits)
+        for (int r = 0; r < cnt_l; ++r) raw[roff + r] = mine[r];
+      Piece& pc = out[pidx];
+      pc.q = fits ? roff : -1;
+      pc.row = row_l;
+      pc.nrows = cnt_l;
+      pc.key = -1;
+      pc.kind = PIECE_RAW;
+    }
+    return __popc(heads);
   }
 
   // A SAFE piece stores the expected top 12 bits of S (sign | biased exponent) and the
@@ -689,7 +696,7 @@ struct Solver {
       const int blk0 = k * TILE + wid_ * BLK;
       const bool live = blk0 < n_;  // warp-uniform
       const long long te = clock64();
-      if (k >= 2) mbar_wait(&SMX.empty_bar[s], ((k - 2) >> 1) & 1);  // walker done with k-2
+      if (k >= 2) mbar_wait(&SMX.empty_bar[s], ((k - 2) >> 1) & 1);
       if (wid_ == 0 && lane_ == 0) SMX.prof[PR_EMPTY] += clock64() - te;
       int e_pred = 0, ng_pred = 0;
       const bool pred_ok = in_binade(P + (double)wid_ * blk_est, 0.0, e_pred, ng_pred);
@@ -700,28 +707,29 @@ struct Solver {
       double sb = 0.0, sa = 0.0;
       const long long t0 = clock64();
       // -- loads + priced argmax + speculative quanta -----------------------------------
+      // branch-free (rows past the end compute on stale ring bytes and are then zeroed):
+      // a per-row branch would make every row its own basic block and serialise the
+      // unrolled rows' dependency chains instead of interleaving them
       auto row_work = [&](const double* v, const int g, const int j) {
         const bool valid = j < n_;
-        double bj = 0.0;
+        double bj;
         int arg = 0;
-        if (valid) {
-          if (MODE == PASS_EVAL) {
-            bj = __dsub_rn(v[0], a[0]);
+        if (MODE == PASS_EVAL) {
+          bj = __dsub_rn(v[0], a[0]);
 #pragma unroll
-            for (int i = 1; i < MM; ++i) {
-              if (FULLM || i < m_) {
-                const double x = __dsub_rn(v[i], a[i]);
-                if (x > bj) {
-                  bj = x;
-                  arg = i;
-                }
-              }
+          for (int i = 1; i < MM; ++i) {
+            if (FULLM || i < m_) {
+              const double x = __dsub_rn(v[i], a[i]);
+              const bool gt = x > bj;
+              bj = gt ? x : bj;
+              arg = gt ? i : arg;
             }
-          } else {
-            arg = mo_in ? (int)mo_in[j] : 0;
-            bj = v[arg];
           }
+        } else {
+          arg = (mo_in && valid) ? (int)mo_in[j] : 0;
+          bj = v[arg];
         }
+        bj = valid ? bj : 0.0;
         scr[g * 32 + lane_] = bj;
         Q += quanta(bj, scale, tie);
         sb += bj;
@@ -890,14 +898,16 @@ struct Solver {
           if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_FAST], 1ull);
         } else {  // 32-row sub-segments from the smem copy of b
           __syncwarp();
+          const long long tsl = clock64();
           np = slow_block(scr, SMX.raw[s][wid_], blk0, n_, Pw, Aw, out);
           if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_SLOW], 1ull);
+
         }
       }
       if (lane_ == 0) SMX.npieces[s][wid_] = np;
       __syncwarp();
       if (lane_ == 0) {
-        __threadfence_block();  // the warp's pieces / raw values before the release
+        __threadfence_block();
         mbar_arrive(&SMX.full_bar[s]);
       }
       // per-model counts: 16-bit packed lanes, flushed before they can overflow
