@@ -61,9 +61,9 @@ def schedule_params(rw, wl, name, tau):
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled during the timed region, in-process through
-    NVML (nvidia_ml_py) — a per-sample nvidia-smi subprocess measurably disturbs the
-    run; nvidia-smi is the fallback when NVML is unavailable."""
+    """SM clocks and throttle reasons sampled during the timed region through NVML
+    (nvidia_ml_py) from a separate sampler process; an in-process NVML thread is the
+    fallback, nvidia-smi the last resort when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -79,6 +79,9 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
+            # the max SM clock is a constant: query it once, outside the timed region
+            self.max_sm = self.nvml[0].nvmlDeviceGetMaxClockInfo(self.nvml[1],
+                                                                  self.nvml[0].NVML_CLOCK_SM)
         except Exception:
             self.nvml = None
 
@@ -86,7 +89,7 @@ class ClockSampler:
         if self.nvml is not None:
             nv, h = self.nvml
             sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = self.max_sm
             rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             return [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS]
         out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -105,12 +108,37 @@ class ClockSampler:
             self.stop.wait(self.period)
 
     def __enter__(self):
-        self.t.start()
+        # default: a separate sampler process.  An NVML sampling thread inside this process
+        # stalled the host between launches by 30-280 ms per 1 s step (measured on the
+        # B200 box: 1033-1296 ms/step vs 1007 ms of kernel; 1011 ms with the process)
+        mode = os.environ.get("RW_CLK_MODE", "proc" if self.nvml is not None else "thread")
+        if mode == "thread":
+            self.t.start()
+        else:
+            code = ("import pynvml,time,sys\npynvml.nvmlInit()\n"
+                    f"h=pynvml.nvmlDeviceGetHandleByIndex({self.index})\n"
+                    "while True:\n"
+                    " sm=pynvml.nvmlDeviceGetClockInfo(h,pynvml.NVML_CLOCK_SM)\n"
+                    " rs=pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)\n"
+                    " print(sm,rs,flush=True)\n"
+                    f" time.sleep({self.period})\n")
+            self.proc = subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE,
+                                         text=True)
         return self
 
     def __exit__(self, *a):
+        if getattr(self, "proc", None) is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            for ln in out.split("\n"):
+                f = ln.split()
+                if len(f) == 2 and f[0].isdigit() and f[1].isdigit():
+                    rs = int(f[1])
+                    self.samples.append([f[0], str(self.max_sm)] +
+                                        ["Active" if rs & b else "Not Active" for b in self.BITS])
         self.stop.set()
-        self.t.join(timeout=10)
+        if self.t.is_alive():
+            self.t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
@@ -122,7 +150,9 @@ class ClockSampler:
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
+                "samples": len(self.samples),
+                "source": ("nvml" + (", sampler process" if getattr(self, "proc", None) else ""))
+                if self.nvml else "nvidia-smi"}
 
 
 def peak_gbs():

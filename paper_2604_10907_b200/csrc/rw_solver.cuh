@@ -438,13 +438,14 @@ struct Solver {
   __device__ __forceinline__ void walk(int ntiles, const double (&a)[MM], int m_,
                                        const uint8_t* mo_in) {
     const int lane_ = threadIdx.x & 31;
+    const bool prof = jb.prof_out != nullptr;  // diagnostics counters only when asked for
     double S = 0.0;  // valid in lane 0
     long long raw_rows = 0;
     for (int k = 0; k < ntiles; ++k) {
       const int s = k & 1;
-      const long long t0 = clock64();
+      const long long t0 = prof ? clock64() : 0;
       mbar_wait(&SMX.full_bar[s], (k >> 1) & 1);
-      const long long t1 = clock64();
+      const long long t1 = prof ? clock64() : 0;
       for (int w2 = 0; w2 < WP; ++w2) {
         int np = SMX.npieces[s][w2];
         int p = 0;
@@ -496,7 +497,7 @@ struct Solver {
         __threadfence_block();
         mbar_arrive(&SMX.empty_bar[s]);
       }
-      if (lane_ == 0) {
+      if (prof && lane_ == 0) {
         SMX.prof[PR_WALK_WAIT] += t1 - t0;
         SMX.prof[PR_WALK_BUSY] += clock64() - t1;
       }
@@ -664,6 +665,7 @@ struct Solver {
                                           const int m_, const bool want_counts, uint8_t* mo_out,
                                           const uint8_t* mo_in) {
     const int lane_ = threadIdx.x & 31, wid_ = threadIdx.x >> 5;
+    const bool prof = jb.prof_out != nullptr;  // diagnostics counters only when asked for
     const double* __restrict__ sc = jb.scores;
     double* scr = SMX.bscr[wid_];
     // full-width rows: compile-time load shape (the ABI guarantees 32-byte alignment)
@@ -695,9 +697,9 @@ struct Solver {
       const int s = k & 1;
       const int blk0 = k * TILE + wid_ * BLK;
       const bool live = blk0 < n_;  // warp-uniform
-      const long long te = clock64();
+      const long long te = prof ? clock64() : 0;
       if (k >= 2) mbar_wait(&SMX.empty_bar[s], ((k - 2) >> 1) & 1);
-      if (wid_ == 0 && lane_ == 0) SMX.prof[PR_EMPTY] += clock64() - te;
+      if (prof && wid_ == 0 && lane_ == 0) SMX.prof[PR_EMPTY] += clock64() - te;
       int e_pred = 0, ng_pred = 0;
       const bool pred_ok = in_binade(P + (double)wid_ * blk_est, 0.0, e_pred, ng_pred);
       const double scale =
@@ -705,7 +707,7 @@ struct Solver {
       long long Q = 0;
       bool tie = false;
       double sb = 0.0, sa = 0.0;
-      const long long t0 = clock64();
+      const long long t0 = prof ? clock64() : 0;
       // -- loads + priced argmax + speculative quanta -----------------------------------
       // branch-free (rows past the end compute on stale ring bytes and are then zeroed):
       // a per-row branch would make every row its own basic block and serialise the
@@ -858,11 +860,11 @@ struct Solver {
         SMX.tot_b[s][wid_] = sb;
         SMX.tot_a[s][wid_] = sa;
       }
-      const long long t1 = clock64();
+      const long long t1 = prof ? clock64() : 0;
       // all producer warps' totals: a hardware named barrier (waiting warps are parked, not
       // polling an mbarrier and stealing issue slots from the warps still streaming)
       asm volatile("bar.sync 1, %0;" ::"r"(WP * 32) : "memory");
-      const long long t2 = clock64();
+      const long long t2 = prof ? clock64() : 0;
       double Pw = P, Aw = A;
       const double P_prev = P;
 #pragma unroll 1
@@ -876,7 +878,7 @@ struct Solver {
         A += ta;
       }
       blk_est = (P - P_prev) * (1.0 / WP);
-      if (wid_ == 0 && lane_ == 0) {
+      if (prof && wid_ == 0 && lane_ == 0) {
         SMX.prof[PR_LOAD] += t1 - t0;
         SMX.prof[PR_TOTBAR] += t2 - t1;
       }
@@ -895,12 +897,11 @@ struct Solver {
           Q = warp_sum_ll(Q);
           if (lane_ == 0) set_safe(out[0], Q, blk0, nrows, 2 * e0 + n0);
           np = 1;
-          if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_FAST], 1ull);
+          if (prof && lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_FAST], 1ull);
         } else {  // 32-row sub-segments from the smem copy of b
           __syncwarp();
-          const long long tsl = clock64();
           np = slow_block(scr, SMX.raw[s][wid_], blk0, n_, Pw, Aw, out);
-          if (lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_SLOW], 1ull);
+          if (prof && lane_ == 0) atomicAdd((unsigned long long*)&SMX.prof[PR_SLOW], 1ull);
 
         }
       }
