@@ -107,34 +107,48 @@ class ClockSampler:
                 pass
             self.stop.wait(self.period)
 
-    def __enter__(self):
-        # default: a separate sampler process.  An NVML sampling thread inside this process
-        # stalled the host between launches by 30-280 ms per 1 s step (measured on the
-        # B200 box: 1033-1296 ms/step vs 1007 ms of kernel; 1011 ms with the process)
-        mode = os.environ.get("RW_CLK_MODE", "proc" if self.nvml is not None else "thread")
-        if mode == "thread":
-            self.t.start()
-        else:
+    def start(self):
+        """Default: a separate sampler process, started BEFORE the warm-up so its start-up
+        (interpreter, nvmlInit) is outside the timed region; only samples stamped inside
+        the timed region are kept, and no sampling work shares the launching process."""
+        self.mode = os.environ.get("RW_CLK_MODE", "proc" if self.nvml is not None else "thread")
+        self.proc = None
+        if self.mode == "proc":
             code = ("import pynvml,time,sys\npynvml.nvmlInit()\n"
                     f"h=pynvml.nvmlDeviceGetHandleByIndex({self.index})\n"
                     "while True:\n"
                     " sm=pynvml.nvmlDeviceGetClockInfo(h,pynvml.NVML_CLOCK_SM)\n"
                     " rs=pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)\n"
-                    " print(sm,rs,flush=True)\n"
+                    " print(repr(time.time()),sm,rs,flush=True)\n"
                     f" time.sleep({self.period})\n")
             self.proc = subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE,
                                          text=True)
         return self
 
+    def __enter__(self):
+        if not hasattr(self, "mode"):
+            self.start()
+        if self.mode == "thread":
+            self.t.start()
+        self.t_in = time.time()
+        return self
+
     def __exit__(self, *a):
+        t_out = time.time()
         if getattr(self, "proc", None) is not None:
             self.proc.terminate()
             out, _ = self.proc.communicate(timeout=10)
             for ln in out.split("\n"):
                 f = ln.split()
-                if len(f) == 2 and f[0].isdigit() and f[1].isdigit():
-                    rs = int(f[1])
-                    self.samples.append([f[0], str(self.max_sm)] +
+                if len(f) == 3 and f[1].isdigit() and f[2].isdigit():
+                    try:
+                        ts = float(f[0])
+                    except ValueError:
+                        continue
+                    if not (self.t_in <= ts <= t_out):
+                        continue  # outside the timed region
+                    rs = int(f[2])
+                    self.samples.append([f[1], str(self.max_sm)] +
                                         ["Active" if rs & b else "Not Active" for b in self.BITS])
         self.stop.set()
         if self.t.is_alive():
@@ -324,6 +338,13 @@ def main():
             recs.append(eng.sweep_fetch())
         return np.concatenate(recs)
 
+    sampler = ClockSampler(local).start()  # its start-up stays outside the timed region
+    # no Python GC pause may land between two launches of the timed region: measured on the
+    # B200 box, host stalls between launches made ms_per_step vary 1029-1296 ms around a
+    # steady 1007 ms kernel; with the collector off it stays at 1011-1016 ms
+    import gc
+    gc.collect()
+    gc.disable()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -335,7 +356,7 @@ def main():
     # L2 flush between timed steps (timing rule): a 256 MiB write evicts the 126 MB L2, so
     # every step starts with the score matrix in HBM (the flush time is inside the timing)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    with ClockSampler(local) as clk:
+    with sampler as clk:
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -350,6 +371,7 @@ def main():
                 launches += 1
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+    gc.enable()
     local_ms = ev0.elapsed_time(ev1)
     mine = np.concatenate(recs)
     # gather the fixed-size records (one collective) and reduce deterministically
@@ -377,6 +399,8 @@ def main():
         tsum = 0.0
         passes_e2e = 0
         iters = max(1, min(args.steps, 3))
+        gc.collect()
+        gc.disable()  # as for the device-timed loop
         for it in range(iters + 1):
             torch.cuda.synchronize(dev)
             if world > 1:
@@ -397,6 +421,7 @@ def main():
             if it > 0:  # first iteration is warm-up (allocations)
                 tsum += dt
                 passes_e2e = int(r["eval_passes"].sum())
+        gc.enable()
         if world > 1:
             tt = torch.tensor([tsum], dtype=torch.float64, device=cdev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
