@@ -1,20 +1,27 @@
 #!/usr/bin/env python3
 """bench.py — setup x lambda-iter x prompt routing evals/sec of the B200 setup-search path.
 
-Workload (BASELINE.json configs[1]): 100k synthetic prompts x 4 models,
-512 retained setups (tp x rho grid), SLO sweep of 8 targets = 4096 (setup, tau) instances,
-solved by one persistent sm_100a kernel launch per step.  Optimizer schedule: BASELINE.md's
-truncated schedule for C2-C5 (subgradient 20 iters, PGA 5 iters, beta epsilon = span/4) —
-the same schedule the CPU baseline runs (`--schedule default` selects the reference
-defaults).  A "step" = one full sweep of all instances (select_setup per SLO + reduction).
+Workload (BASELINE.json configs[2], SURVEY.md §8d C3 — the config north_star quotes its
+targets on): 1M synthetic prompts x 8 models, all 4096 retained setups (tp x rho grid incl.
+tensor-parallel degrees), tau = 100 ms.  Optimizer schedule: BASELINE.md's truncated schedule
+for C2-C5 (subgradient 20 iters, PGA 5 iters, beta epsilon = span/4) — the schedule the CPU
+baseline runs on the same inputs (`--schedule default` selects the reference defaults).
+A "step" = one full select_setup: every retained setup solved on the GPU(s), the records
+combined and reduced to the optimal setup (so ms_per_step = wall time to the optimal setup).
 
 Unit of work: one eval = one prompt's priced argmax for one (setup, price
-iterate), i.e. one row of one eval_dual pass; evals/s = sum(eval passes) * N / time.
-Multi-GPU: instances are interleaved over ranks (no data-path collective); one NCCL
-all_gather of the fixed-size per-instance records feeds the order-deterministic reduction.
+iterate), i.e. one row of one eval_dual pass; evals/s = executed eval passes * N / time.
+Passes the GPU did not execute (the memoised first PGA solve, identical for every setup)
+are not counted.
+
+Multi-GPU (strong scaling, the north_star's fixed 4096-setup sweep): instances are
+interleaved over the ranks (no data-path collective); each rank's kernel writes its
+fixed-size records into a padded device buffer and ONE NCCL all_gather_into_tensor
+combines them for the order-deterministic reduction.  Time = max over ranks.
 
 Arms: default = ours (librw_b200.so); `--impl reference` = the reference's own CPU
-select_setup (oracle/_ref, compiled from /root/reference sources) on a bounded sample.
+select_setup (oracle/_ref, compiled from /root/reference sources), inputs built by the
+reference library's own synth_scores / enumerate+retain, on a bounded sample.
 """
 from __future__ import annotations
 
@@ -32,11 +39,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
-TRAFFIC = os.path.join(ROOT, "profiles", "traffic_r01.json")
-PASS_FIXTURE = os.path.join(ROOT, "tests", "golden", "bench_sample_passes.json")
 METRIC = "setup×λ-iter×prompt routing evals/sec; wall time to optimal setup (1/2/4/8 GPU)"
-SAMPLE_SETUPS = 64   # CPU sample: the first 64 retained setups of the workload ...
-SAMPLE_TAU = 120.0   # ... at one SLO
+TRAFFIC_FILES = [os.path.join(ROOT, "profiles", f) for f in
+                 ("traffic_r02.json", "traffic_r01.json")]
 
 
 def parse():
@@ -45,7 +50,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--schedule", default="truncated", choices=["truncated", "default"])
     ap.add_argument("--n", type=int, default=None, help="override prompt count (debug)")
     ap.add_argument("--setups", type=int, default=None, help="limit retained setups (debug)")
@@ -54,230 +59,249 @@ def parse():
     return ap.parse_args()
 
 
-def schedule_params(rw, wl, name, tau):
+# ---- shared between the two arms ---------------------------------------------------------
+def sweep_params(rw_or_wl, wl, name, tau):
     if name == "default":
-        return rw.BetaSearchParams()
+        return wl.rp.BetaSearchParams()
     return wl.with_span_epsilon(wl.truncated_params(), tau, 4.0)
 
 
-class ClockSampler:
-    """SM clocks and throttle reasons sampled during the timed region through NVML
-    (nvidia_ml_py) from a separate sampler process; an in-process NVML thread is the
-    fallback, nvidia-smi the last resort when NVML is unavailable."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
-    # NVML clocks-event-reason bits: hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
-    BITS = [0x8, 0x40, 0x20, 0x4]
-
-    def __init__(self, index, period=0.25):
-        self.index, self.period, self.samples, self.stop = index, period, [], threading.Event()
-        self.t = threading.Thread(target=self.run, daemon=True)
-        self.nvml = None
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(index))
-            # the max SM clock is a constant: query it once, outside the timed region
-            self.max_sm = self.nvml[0].nvmlDeviceGetMaxClockInfo(self.nvml[1],
-                                                                  self.nvml[0].NVML_CLOCK_SM)
-        except Exception:
-            self.nvml = None
-
-    def sample(self):
-        if self.nvml is not None:
-            nv, h = self.nvml
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            mx = self.max_sm
-            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            return [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in self.BITS]
-        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                              "--format=csv,noheader,nounits"],
-                             capture_output=True, text=True, timeout=5).stdout.strip()
-        return [x.strip() for x in out.split(",")] if out else None
-
-    def run(self):
-        while not self.stop.is_set():
-            try:
-                smp = self.sample()
-                if smp:
-                    self.samples.append(smp)
-            except Exception:
-                pass
-            self.stop.wait(self.period)
-
-    def start(self):
-        """Default: a separate sampler process, started BEFORE the warm-up so its start-up
-        (interpreter, nvmlInit) is outside the timed region; only samples stamped inside
-        the timed region are kept, and no sampling work shares the launching process."""
-        self.mode = os.environ.get("RW_CLK_MODE", "proc" if self.nvml is not None else "thread")
-        self.proc = None
-        if self.mode == "proc":
-            code = ("import pynvml,time,sys\npynvml.nvmlInit()\n"
-                    f"h=pynvml.nvmlDeviceGetHandleByIndex({self.index})\n"
-                    "while True:\n"
-                    " sm=pynvml.nvmlDeviceGetClockInfo(h,pynvml.NVML_CLOCK_SM)\n"
-                    " rs=pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)\n"
-                    " print(repr(time.time()),sm,rs,flush=True)\n"
-                    f" time.sleep({self.period})\n")
-            self.proc = subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE,
-                                         text=True)
-        return self
-
-    def __enter__(self):
-        if not hasattr(self, "mode"):
-            self.start()
-        if self.mode == "thread":
-            self.t.start()
-        self.t_in = time.time()
-        return self
-
-    def __exit__(self, *a):
-        t_out = time.time()
-        if getattr(self, "proc", None) is not None:
-            self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=10)
-            for ln in out.split("\n"):
-                f = ln.split()
-                if len(f) == 3 and f[1].isdigit() and f[2].isdigit():
-                    try:
-                        ts = float(f[0])
-                    except ValueError:
-                        continue
-                    if not (self.t_in <= ts <= t_out):
-                        continue  # outside the timed region
-                    rs = int(f[2])
-                    self.samples.append([f[1], str(self.max_sm)] +
-                                        ["Active" if rs & b else "Not Active" for b in self.BITS])
-        self.stop.set()
-        if self.t.is_alive():
-            self.t.join(timeout=10)
-
-    def summary(self):
-        if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples),
-                "source": ("nvml" + (", sampler process" if getattr(self, "proc", None) else ""))
-                if self.nvml else "nvidia-smi"}
+def sample_spec(cfg):
+    """The CPU sample: the first S retained setups of the workload at one SLO.  Enumeration
+    is model-major (model 0 most significant, setup_search.cpp:99-125), so fixing the leading
+    models to their first choice enumerates exactly the first S setups, same order, same
+    ordinals.  S is the largest trailing choice product <= the budget (16 setups at 1M
+    prompts, 64 below)."""
+    budget = 16 if cfg.n * cfg.m >= 4_000_000 else 64
+    counts = [len(t) * len(r) for t, r in zip(cfg.tp_choices, cfg.rho_choices)]
+    prod, fixed = 1, cfg.m
+    while fixed > 0 and prod * counts[fixed - 1] <= budget:
+        prod *= counts[fixed - 1]
+        fixed -= 1
+    tau = cfg.taus[min(3, len(cfg.taus) - 1)]
+    return prod, fixed, tau
 
 
-def peak_gbs():
-    try:
-        with open(PEAKS) as f:
-            return float(json.load(f)["hbm_gbs"]), "measured"
-    except Exception:
-        return 6650.0, "fallback"
+def config_dict(cfg, n_setups, taus, schedule, world, sample):
+    S, fixed, tau = sample
+    return {"workload": cfg.name, "instances": n_setups * len(taus), "setups": n_setups,
+            "slo_targets_ms": [float(t) for t in taus], "n_prompts": cfg.n,
+            "n_models": cfg.m, "schedule": schedule,
+            "parallelism": f"setup-sharded x{world} (strong scaling: fixed sweep)",
+            "l2": "flushed before every timed step (256 MiB write); the 8*N*M-byte matrix "
+                  "is then re-read from L2/HBM on every eval pass",
+            "cpu_sample": f"reference select_setup over the first {S} retained setups "
+                          f"(models 0..{fixed - 1} at their first choice) at tau={tau}"}
 
 
-def cpu_sample(cfg, inp, s, params, tau):
-    """Setup-space restriction whose enumeration is exactly the first SAMPLE_SETUPS
-    retained setups of the workload (model 0 is the most significant digit)."""
-    per0 = len(inp.retained) // (len(cfg.tp_choices[0]) * len(cfg.rho_choices[0]))
-    take0 = max(1, SAMPLE_SETUPS // max(per0, 1))
-    choices0 = [(tp, r) for tp in cfg.tp_choices[0] for r in cfg.rho_choices[0]][:take0]
-    return choices0
+class RefSpace:
+    pass
 
 
-def run_reference_select(cfg, inp, s, p, tau, threads):
-    """Time oracle/_ref select_setup on the bounded sample; returns (seconds, retained)."""
+def ref_space(cfg, inp, fixed, tau):
+    """Restricted setup space for the reference's select_setup (see sample_spec)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from oracle import Params, ProfileTable, Reference  # the reference arm / cpu_baseline
-    R = Reference()
-
-    class Space:
-        pass
-
-    sp = Space()
-    ch0 = cpu_sample(cfg, inp, s, p, tau)
-    tps0 = sorted({c[0] for c in ch0})
-    rhos0 = sorted({c[1] for c in ch0})
-    sp.tp_choices = [tps0] + [list(t) for t in cfg.tp_choices[1:]]
-    sp.rho_choices = [rhos0] + [list(r) for r in cfg.rho_choices[1:]]
+    from oracle import ProfileTable
+    sp = RefSpace()
+    sp.tp_choices = [[t[0]] if i < fixed else list(t) for i, t in enumerate(cfg.tp_choices)]
+    sp.rho_choices = [[r[0]] if i < fixed else list(r) for i, r in enumerate(cfg.rho_choices)]
     sp.memory = [(cfg.models.index(mdl), tp, f) for (mdl, tp), f in cfg.mem.items()]
     sp.profile_keys = inp.profile_keys
     sp.profiles = ProfileTable(inp.koff, inp.kx, inp.ky)
     sp.gpu_count, sp.rho_floor = cfg.gpu_count, cfg.rho_floor
     sp.lambda_rps, sp.tau_ms, sp.kappa = cfg.lambda_rps, tau, cfg.kappa
+    return sp
+
+
+def ref_params(p):
+    from oracle import Params
     d = p.pga.dual
-    op = Params(eta0=d.eta0, sub_max_iters=d.max_iters, residual_tol=d.residual_tol,
-                polish_passes=d.polish_passes, pga_eta=p.pga.eta, pga_max_iters=p.pga.max_iters,
-                w_tol=p.pga.w_tol, beta_min=p.beta_min, beta_max=p.beta_max, epsilon=p.epsilon)
-    t0 = time.perf_counter()
-    out = R.select_setup(s, sp, op, parallelism=threads)
-    dt = time.perf_counter() - t0
-    return dt, out
+    return Params(eta0=d.eta0, sub_max_iters=d.max_iters, residual_tol=d.residual_tol,
+                  polish_passes=d.polish_passes, pga_eta=p.pga.eta,
+                  pga_max_iters=p.pga.max_iters, w_tol=p.pga.w_tol, beta_min=p.beta_min,
+                  beta_max=p.beta_max, epsilon=p.epsilon)
 
 
-def sample_passes_from_fixture(cfg, schedule, n_sample):
+def cpu_model():
     try:
-        with open(PASS_FIXTURE) as f:
-            fx = json.load(f)
-        key = f"{cfg.name}|n={cfg.n}|{schedule}|tau={SAMPLE_TAU}"
-        if key in fx and len(fx[key]) >= n_sample:
-            return int(sum(fx[key][:n_sample]))
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
     except Exception:
         pass
-    return None
+    return "unknown"
 
 
+def count_passes(cfg, inp, s, sample, p, schedule):
+    """eval_dual passes of the reference trajectory on the sample.  From the committed
+    protocol fixture of this workload when it covers the sample (tests/golden/protocol_*.json,
+    made through the reference library by tests/golden/gen_protocol.py), else counted with the
+    C restatement (pinned to the reference; untimed — the trajectories are bit-identical)."""
+    S, _, tau = sample
+    key = cfg.name.split(":")[0]
+    path = os.path.join(ROOT, "tests", "golden", f"protocol_{key}.json")
+    try:
+        with open(path) as f:
+            g = json.load(f)
+        if g["n"] == cfg.n and g["schedule"] == schedule:
+            for sl in g["slos"]:
+                if sl["tau"] == tau and len(sl["oracle"]) >= S:
+                    return sum(int(r["eval_passes"]) for r in sl["oracle"][:S])
+    except Exception:
+        pass
+    from oracle import Oracle, ProfileTable
+    O = Oracle()
+    prof = ProfileTable(inp.koff, inp.kx, inp.ky)
+    op = ref_params(p)
+    return sum(O.evaluate_setup(s, prof, inp.profile_index[k], cfg.lambda_rps, tau, cfg.kappa,
+                                op)["eval_passes"] for k in range(S))
+
+
+# ---- clocks ------------------------------------------------------------------------------
+class ClockSampler:
+    """SM clocks and throttle reasons sampled during the timed region through NVML
+    (nvidia_ml_py) from a separate sampler process started before the warm-up; only samples
+    stamped inside the timed region are kept."""
+
+    BITS = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+
+    def __init__(self, index, period=0.25):
+        self.index, self.period, self.samples = index, period, []
+        self.proc, self.max_sm = None, None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.max_sm = None
+
+    def start(self):
+        code = ("import pynvml,time\npynvml.nvmlInit()\n"
+                f"h=pynvml.nvmlDeviceGetHandleByIndex({self.index})\n"
+                "while True:\n"
+                " sm=pynvml.nvmlDeviceGetClockInfo(h,pynvml.NVML_CLOCK_SM)\n"
+                " rs=pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)\n"
+                " print(repr(time.time()),sm,rs,flush=True)\n"
+                f" time.sleep({self.period})\n")
+        try:
+            self.proc = subprocess.Popen([sys.executable, "-c", code], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __enter__(self):
+        self.t_in = time.time()
+        return self
+
+    def __exit__(self, *a):
+        t_out = time.time()
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for ln in out.split("\n"):
+            f = ln.split()
+            if len(f) == 3 and f[1].isdigit() and f[2].isdigit():
+                try:
+                    ts = float(f[0])
+                except ValueError:
+                    continue
+                if self.t_in <= ts <= t_out:
+                    self.samples.append((int(f[1]), int(f[2])))
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, rs in self.samples for i in range(4)
+                          if rs & self.BITS[i]})
+        return {"sm_mhz": float(np.median([s for s, _ in self.samples])),
+                "sm_max_mhz": self.max_sm, "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml, sampler process"}
+
+
+def peak_gbs():
+    try:
+        with open(PEAKS) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 7672.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_for(cfg, schedule):
+    """ncu dram__bytes_read+write of the solver kernel per launch, from the committed
+    profiles/ capture of this same workload and schedule (null if not captured)."""
+    for path in TRAFFIC_FILES:
+        try:
+            with open(path) as f:
+                tr = json.load(f)
+        except Exception:
+            continue
+        for e in (tr if isinstance(tr, list) else [tr]):
+            if e.get("workload") == cfg.name and e.get("schedule") == schedule:
+                return e.get("dram_bytes_per_launch"), os.path.relpath(path, ROOT)
+    return None, None
+
+
+# ---- the reference arm -------------------------------------------------------------------
 def reference_arm(args):
-    from paper_2604_10907_b200 import routeplan as rp  # input producers (host C++)
-    from paper_2604_10907_b200 import workloads as wl
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Reference
+    from paper_2604_10907_b200 import workloads as wl  # pure-Python workload description
+    R = Reference()
     cfg = wl.config(args.workload, args.n)
-    inp = wl.build_inputs(cfg, limit=args.setups)
-    s = wl.scores_for(cfg)
-    p = schedule_params(rp, wl, args.schedule, SAMPLE_TAU)
+    # inputs from the reference library's own producers: nothing of ours is loaded
+    inp = wl.build_inputs(cfg, limit=args.setups, enumerate_fn=R.enumerate_retain)
+    s = wl.scores_for(cfg, synth=R.synth_scores)
+    sample = sample_spec(cfg)
+    S, fixed, tau = sample
+    p = sweep_params(None, wl, args.schedule, tau)
+    op = ref_params(p)
     threads = os.cpu_count() or 1
+    sp = ref_space(cfg, inp, fixed, tau)
+    # warm-up: one setup of the same shape at N/100 (pages the library and inputs in)
+    small = wl.config(args.workload, max(1000, cfg.n // 100))
+    s_small = wl.scores_for(small, synth=R.synth_scores)
+    sp_small = ref_space(small, inp, cfg.m, tau)
     for _ in range(args.warmup):
-        run_reference_select(cfg, inp, s, p, SAMPLE_TAU, threads)
-    times = []
-    out = None
+        R.select_setup(s_small, sp_small, op, parallelism=threads)
+    times, out = [], None
+    import gc
+    gc.disable()
     for _ in range(args.steps):
-        dt, out = run_reference_select(cfg, inp, s, p, SAMPLE_TAU, threads)
-        times.append(dt)
-    n_sample = out["retained"]
-    passes = sample_passes_from_fixture(cfg, args.schedule, n_sample)
-    if passes is None:  # count with the C restatement (untimed; bit-identical trajectories)
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        from oracle import Oracle, Params, ProfileTable
-        O = Oracle()
-        prof = ProfileTable(inp.koff, inp.kx, inp.ky)
-        d = p.pga.dual
-        op = Params(eta0=d.eta0, sub_max_iters=d.max_iters, residual_tol=d.residual_tol,
-                    polish_passes=d.polish_passes, pga_eta=p.pga.eta,
-                    pga_max_iters=p.pga.max_iters, w_tol=p.pga.w_tol, beta_min=p.beta_min,
-                    beta_max=p.beta_max, epsilon=p.epsilon)
-        passes = sum(O.evaluate_setup(s, prof, inp.profile_index[k], cfg.lambda_rps, SAMPLE_TAU,
-                                      cfg.kappa, op)["eval_passes"] for k in range(n_sample))
+        t0 = time.perf_counter()
+        out = R.select_setup(s, sp, op, parallelism=threads)
+        times.append(time.perf_counter() - t0)
+    gc.enable()
+    assert out["retained"] == S, (out["retained"], S)
+    passes = count_passes(cfg, inp, s, sample, p, args.schedule)
     t = float(np.mean(times))
     v = passes * cfg.n / t
+    n_setups = len(inp.retained)
     line = {"metric": METRIC, "value": v, "unit": "evals/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}; CPU sample: first {n_sample} setups at "
-                                   f"tau={SAMPLE_TAU}",
-                       "schedule": args.schedule, "n_prompts": cfg.n, "n_models": cfg.m},
+            "config": config_dict(cfg, n_setups, cfg.taus, args.schedule, world, sample),
             "cpu_baseline": {"value": v, "unit": "evals/s", "cores": threads,
-                             "kind": "reference",
-                             "sample": f"select_setup over the first {n_sample} retained setups "
-                                       f"at tau={SAMPLE_TAU}, parallelism={threads}"},
+                             "kind": "reference", "cpu_model": cpu_model(),
+                             "sample": f"each step: reference select_setup over the first "
+                                       f"{S} retained setups at tau={tau}, "
+                                       f"parallelism={threads}, {passes} eval passes; "
+                                       f"warm-up steps: 1 setup at N={small.n}"},
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ---- our arm -----------------------------------------------------------------------------
 def main():
     args = parse()
     if args.impl == "reference":
@@ -301,23 +325,20 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cdev = torch.device("cpu") if shared else dev  # device the collectives run on
 
     import paper_2604_10907_b200 as rw
-    from paper_2604_10907_b200 import _abi
+    from paper_2604_10907_b200 import shard
     from paper_2604_10907_b200 import workloads as wl
 
     cfg = wl.config(args.workload, args.n)
     inp = wl.build_inputs(cfg, limit=args.setups)
     s_host = wl.scores_for(cfg)
-    # weak scaling (contract: the path partitions, per-GPU work fixed as N grows): at N
-    # ranks the SLO sweep has 8*N targets — N copies of C2's 8, copy c offset by 0.5*c ms —
-    # interleaved over the ranks, so every GPU solves ~4096 (setup, tau) instances
-    taus = np.array([t + 0.5 * c for c in range(world) for t in cfg.taus], np.float64)
+    taus = np.array(cfg.taus, np.float64)  # strong scaling: the same sweep at every N
     S = len(inp.retained)
     n_inst = S * len(taus)
-    p = schedule_params(rw, wl, args.schedule, float(taus[0]))
+    plist = [sweep_params(rw, wl, args.schedule, float(t)) for t in taus]
     opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=float(taus[0]), kappa=cfg.kappa)
+    sample = sample_spec(cfg)
 
     eng = rw.Engine(local)
     stream = torch.cuda.current_stream(dev)
@@ -325,37 +346,41 @@ def main():
     scores_dev = torch.from_numpy(s_host).to(dev)
     eng.bind_scores_device(scores_dev.data_ptr(), cfg.n, cfg.m)
     eng.load_profiles(inp.koff, inp.kx, inp.ky)
+    # the kernel writes this rank's records straight into a padded device buffer, which ONE
+    # all_gather_into_tensor exchanges (NCCL over NVLink; gloo only under the test hook)
+    recbuf, cap = shard.device_record_buffer(n_inst, world, dev)
+    eng.set_records_device(recbuf.data_ptr(), cap)
+    gbuf = recbuf if not shared else None
 
-    def groups():
-        # one launch for all (setup, tau) instances; per-SLO params (truncated epsilon is
-        # span/4 of each SLO's default bracket)
-        return [(taus, [schedule_params(rw, wl, args.schedule, float(t)) for t in taus])]
+    def combine():
+        """records of every rank -> (all records, winner per SLO)"""
+        if world > 1 and not shared:
+            allrec = shard.gather_device_records(recbuf)
+        elif world > 1:
+            allrec = shard.gather_records(eng.sweep_fetch(), n_inst)
+        else:
+            allrec = eng.sweep_fetch()
+        return allrec, shard.winners_per_slo(allrec, [float(t) for t in taus])
 
     def step():
-        recs = []
-        for tg, pg in groups():
-            eng.sweep_async(inp.profile_index, inp.retained, opt, pg, rank, world, taus=tg)
-            recs.append(eng.sweep_fetch())
-        return np.concatenate(recs)
+        shard.reset_device_records(recbuf)
+        eng.sweep_async(inp.profile_index, inp.retained, opt, plist, rank, world, taus=taus)
+        return combine()
 
     sampler = ClockSampler(local).start()  # its start-up stays outside the timed region
-    # no Python GC pause may land between two launches of the timed region: measured on the
-    # B200 box, host stalls between launches made ms_per_step vary 1029-1296 ms around a
-    # steady 1007 ms kernel; with the collector off it stays at 1011-1016 ms
     import gc
     gc.collect()
-    gc.disable()
+    gc.disable()  # no collector pause between two launches of the timed region
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kernel_ms = 0.0
-    launches = 0
     # L2 flush between timed steps (timing rule): a 256 MiB write evicts the 126 MB L2, so
     # every step starts with the score matrix in HBM (the flush time is inside the timing)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms, launches = 0.0, 0
     with sampler as clk:
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -363,29 +388,23 @@ def main():
         ev0.record(stream)
         for _ in range(args.steps):
             flush.fill_(1)
-            recs = []
-            for tg, pg in groups():
-                eng.sweep_async(inp.profile_index, inp.retained, opt, pg, rank, world, taus=tg)
-                recs.append(eng.sweep_fetch())
-                kernel_ms += eng.last_kernel_ms()
-                launches += 1
+            allrec, winners = step()
+            kernel_ms += eng.last_kernel_ms()
+            launches += 1
         ev1.record(stream)
         torch.cuda.synchronize(dev)
     gc.enable()
     local_ms = ev0.elapsed_time(ev1)
-    mine = np.concatenate(recs)
-    # gather the fixed-size records (one collective) and reduce deterministically
-    from paper_2604_10907_b200 import shard
     if world > 1:
-        allrec = shard.gather_records(mine, device=cdev)
-        tt = torch.tensor([local_ms, kernel_ms], dtype=torch.float64, device=cdev)
+        tt = torch.tensor([local_ms, kernel_ms], dtype=torch.float64,
+                          device=torch.device("cpu") if shared else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)  # time = max over ranks
         step_ms = float(tt[0].item()) / args.steps
         kern_ms = float(tt[1].item()) / args.steps
     else:
-        allrec = mine
         step_ms = local_ms / args.steps
         kern_ms = kernel_ms / args.steps
+
     # end to end through the C-ABI with host buffers: every step H2D-copies the matrix and
     # tables from pinned memory, sweeps this rank's shard, D2H-reads the records and (N>1)
     # all-gathers them for the reduction; time = max over ranks
@@ -395,12 +414,10 @@ def main():
         eng2 = rw.Engine(local)
         h2d = pinned.nbytes + inp.koff.nbytes + inp.kx.nbytes + inp.ky.nbytes + \
             inp.profile_index.nbytes + inp.retained.nbytes + taus.nbytes
-        d2h = 0
-        tsum = 0.0
-        passes_e2e = 0
-        iters = max(1, min(args.steps, 3))
+        d2h, tsum, passes_e2e = 0, 0.0, 0
+        iters = max(1, min(args.steps, 2))
         gc.collect()
-        gc.disable()  # as for the device-timed loop
+        gc.disable()
         for it in range(iters + 1):
             torch.cuda.synchronize(dev)
             if world > 1:
@@ -408,22 +425,20 @@ def main():
             t0 = time.perf_counter()
             eng2.load_scores(pinned)
             eng2.load_profiles(inp.koff, inp.kx, inp.ky)
-            recs = []
-            for tg, pg in groups():
-                recs.append(eng2.sweep_slo(inp.profile_index, inp.retained, tg, opt, pg,
-                                           rank, world))
-            r = np.concatenate(recs)
+            r = eng2.sweep_slo(inp.profile_index, inp.retained, taus, opt, plist, rank, world)
             d2h = r.nbytes
             if world > 1:
-                r = shard.gather_records(r, device=cdev)
+                r = shard.gather_records(r, n_inst, device=torch.device("cpu") if shared
+                                         else dev)
             shard.winners_per_slo(r, [float(t) for t in taus])
             dt = time.perf_counter() - t0
-            if it > 0:  # first iteration is warm-up (allocations)
+            if it > 0:  # the first iteration is the warm-up (allocations)
                 tsum += dt
-                passes_e2e = int(r["eval_passes"].sum())
+                passes_e2e = int(r["exec_passes"].sum())
         gc.enable()
         if world > 1:
-            tt = torch.tensor([tsum], dtype=torch.float64, device=cdev)
+            tt = torch.tensor([tsum], dtype=torch.float64,
+                              device=torch.device("cpu") if shared else dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tsum = float(tt[0].item())
         e2e = {"value": passes_e2e * cfg.n / (tsum / iters), "unit": "evals/s",
@@ -431,7 +446,6 @@ def main():
                "ms_per_step": tsum / iters * 1e3}
         eng2.close()
 
-    passes_total = int(allrec["eval_passes"].sum())
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -439,74 +453,69 @@ def main():
         return
     assert len(allrec) == n_inst, (len(allrec), n_inst)
     assert not allrec["status"].any(), "device status error"
+    passes_total = int(allrec["exec_passes"].sum())
+    passes_ref = int(allrec["eval_passes"].sum())
     evals_step = passes_total * cfg.n
     value = evals_step / (step_ms / 1e3)
-    # winner per SLO (wall time to optimal setup = one step for the whole SLO sweep)
-    winners = {str(t): (int(allrec[i]["setup_id"]) if i >= 0 else None)
-               for t, i in shard.winners_per_slo(allrec, [float(t) for t in taus]).items()}
+    win = {str(t): (int(allrec[i]["setup_id"]) if i >= 0 else None) for t, i in winners.items()}
 
-    # roofline of the solver kernel: algorithmic bytes = 8*M per eval
+    # roofline of the solver kernel: algorithmic bytes = 8*M per eval, over the
+    # kernel's device time per step (CUDA events on its launch stream); per GPU
     peak, peak_kind = peak_gbs()
     achieved = evals_step * 8 * cfg.m / (kern_ms / 1e3) / 1e9 / max(world, 1)
-    traffic = None
-    try:
-        with open(TRAFFIC) as f:
-            tr = json.load(f)
-        if tr.get("workload") == cfg.name and tr.get("schedule") == args.schedule:
-            traffic = tr.get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic, traffic_src = traffic_for(cfg, args.schedule)
 
     cpu = None
     if not args.no_cpu and world == 1:
         try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from oracle import Reference
+            R = Reference()
+            S_, fixed, tau = sample
+            p0 = sweep_params(rw, wl, args.schedule, tau)
             threads = os.cpu_count() or 1
-            p0 = schedule_params(rw, wl, args.schedule, SAMPLE_TAU)
-            dt, out = run_reference_select(cfg, inp, s_host, p0, SAMPLE_TAU, threads)
-            n_sample = out["retained"]
-            ti = int(np.nonzero(taus == SAMPLE_TAU)[0][0]) if SAMPLE_TAU in taus else None
-            if ti is not None:
-                sel = allrec[(allrec["tau_ms"] == SAMPLE_TAU)]
-                sel = np.sort(sel, order="setup_id")[:n_sample]
-                sp = int(sel["eval_passes"].sum())
-                # the reference is bit-identical: its sweep records must equal ours
-                same = (np.array_equal(out["sweep_id"], sel["setup_id"]) and
-                        np.array_equal(out["sweep_score"], sel["score"]) and
-                        np.array_equal(out["sweep_latency"], sel["latency_ms"]))
-            else:
-                sp, same = None, None
-            cpu = {"value": (sp * cfg.n / dt) if sp else None, "unit": "evals/s",
-                   "cores": threads, "kind": "reference",
-                   "sample": f"reference select_setup (oracle/_ref) over the first {n_sample} "
-                             f"retained setups at tau={SAMPLE_TAU}, parallelism={threads}, "
-                             f"{dt:.2f}s; records bit-identical to ours: {same}"}
+            t0 = time.perf_counter()
+            out = R.select_setup(s_host, ref_space(cfg, inp, fixed, tau), ref_params(p0),
+                                 parallelism=threads)
+            dt = time.perf_counter() - t0
+            sel = allrec[allrec["tau_ms"] == tau]
+            sel = np.sort(sel, order="setup_id")[:S_]
+            sp = int(sel["eval_passes"].sum())  # == the reference trajectory's passes
+            same = (out["retained"] == S_ and
+                    np.array_equal(out["sweep_id"], sel["setup_id"]) and
+                    np.array_equal(out["sweep_score"].view(np.int64),
+                                   sel["score"].view(np.int64)) and
+                    np.array_equal(out["sweep_latency"].view(np.int64),
+                                   sel["latency_ms"].view(np.int64)) and
+                    np.array_equal(out["sweep_feasible"].astype(bool), sel["feasible"] != 0))
+            cpu = {"value": sp * cfg.n / dt, "unit": "evals/s", "cores": threads,
+                   "kind": "reference", "cpu_model": cpu_model(),
+                   "sample": f"reference select_setup (oracle/_ref) over the first {S_} "
+                             f"retained setups at tau={tau}, parallelism={threads}, "
+                             f"{sp} eval passes in {dt:.2f}s; records bit-identical to this "
+                             f"run's: {same}"}
         except Exception as ex:  # the checker library may be absent on a stripped box
-            cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"unavailable: {type(ex).__name__}: {ex}"}
+            cpu = {"value": None, "unit": "evals/s", "cores": os.cpu_count(),
+                   "kind": "reference", "sample": f"unavailable: {type(ex).__name__}: {ex}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-        "higher_is_better": True, "scaling": "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "instances": n_inst, "setups": S,
-                   "slo_targets_ms": [float(t) for t in taus], "n_prompts": cfg.n,
-                   "n_models": cfg.m, "schedule": args.schedule,
-                   "parallelism": f"setup-sharded x{world}",
-                   "weak_scaling": "8*N SLO targets (C2's 8, replicated with +0.5 ms offsets "
-                                   "per extra GPU); ~4096 instances per GPU",
-                   "l2": "flushed before every timed step (256 MiB write); the matrix is then "
-                         "re-read from L2 on every eval pass",
-                   "winner_setup_per_slo": winners},
+        "config": config_dict(cfg, S, taus, args.schedule, world, sample),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "note": f"algorithmic 8*M bytes per eval over solver-kernel time; peak "
-                             f"{peak_kind} hbm_gbs"},
+                     "note": f"algorithmic 8*M bytes per executed eval over the solver "
+                             f"kernel's event time per step, per GPU; peak {peak_kind}; "
+                             f"traffic = ncu dram bytes per launch from {traffic_src}"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
         "kernel_ms_per_step": kern_ms,
         "eval_passes_per_step": passes_total,
+        "reference_trajectory_passes_per_step": passes_ref,
+        "winner_setup_per_slo": win,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

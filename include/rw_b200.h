@@ -4,15 +4,15 @@
  * torch types.  Every entry point replaces one function of the reference C++ solver
  * API (/root/reference/proj/include/routeplan/...); the replaced interface is cited on
  * each declaration.  INTEGRATION.md shows the C++ forwarding shim a maintainer adds so
- * the reference's host code (runner.cpp:160-172 `run_search`) links against this.
+ * the reference's host code (runner.cpp:46-58 `run_search`) links against this.
  *
  * Conventions
  *  - scores: row-major N x M doubles, `scores[j * M + i]` (workload.hpp:15).
  *  - model order is the score-matrix column order (setup_search.cpp:160-161).
  *  - latency profiles: CSR table; profile p has knots [knot_offsets[p], knot_offsets[p+1])
- *    with strictly increasing load, first load 0 after ingestion (latency.cpp:375-393).
+ *    with strictly increasing load, first load 0 after ingestion (latency.cpp:82-138, anchored at :133-134).
  *    A setup names one profile per model (`profile_index[k * M + i]`), i.e. the
- *    (model, tp, round(rho*1e4), metric) key lookup of latency.cpp:12,331 is resolved by
+ *    (model, tp, round(rho*1e4), metric) key lookup of latency.cpp:12, 60-62 is resolved by
  *    the host before the call.
  *  - all calls are synchronous w.r.t. the host unless stated; results are bit-identical to
  *    the reference CPU solver.
@@ -46,7 +46,7 @@ typedef enum {
 
 typedef struct rw_ctx rw_ctx; /* owns device buffers + a stream on one GPU */
 
-/* score_dual.hpp:46-52 SubgradientParams (init_alpha passed separately). */
+/* score_dual.hpp:41-47 SubgradientParams (init_alpha passed separately). */
 typedef struct {
   double eta0;
   int32_t max_iters;
@@ -62,7 +62,7 @@ typedef struct {
   rw_subgradient_params dual;
 } rw_pga_params;
 
-/* routing_opt.hpp:69-74 BetaSearchParams. */
+/* routing_opt.hpp:60-65 BetaSearchParams. */
 typedef struct {
   double beta_min;
   double beta_max; /* < 0 -> 10 / tau */
@@ -103,7 +103,7 @@ typedef struct {
   int64_t eval_passes;
 } rw_relaxed_result;
 
-/* routing_opt.hpp:57-62 BetaStep. */
+/* routing_opt.hpp:53-58 BetaStep. */
 typedef struct {
   double beta;
   double score;
@@ -138,9 +138,11 @@ typedef struct {
   double w[RW_MAX_MODELS];
   uint32_t out_of_range;
   int32_t bisect_steps;
-  int64_t eval_passes;
+  int64_t eval_passes;   /* eval_dual passes of the reference's trajectory (parity) */
   int64_t polish_passes;
   int64_t repair_calls;
+  int64_t exec_passes;   /* eval passes the GPU executed (memoised solves excluded);
+                            the throughput metric counts these */
 } rw_setup_record;
 
 /* ---- lifecycle ------------------------------------------------------------------- */
@@ -172,23 +174,32 @@ int rw_load_scores(rw_ctx* ctx, int32_t n, int32_t m, const double* host_scores)
 /* Borrow an already-resident device matrix (caller keeps it alive). */
 int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* device_scores);
 /* Upload the latency profile table (replaces ProfileLibrary, latency.hpp:36-42;
- * validated like LatencyProfile::validate, latency.cpp:296-308). */
+ * validated like LatencyProfile::validate, latency.cpp:39-51). */
 int rw_load_profiles(rw_ctx* ctx, int32_t n_profiles, const int64_t* knot_offsets,
                      const double* knot_load, const double* knot_latency);
 
 /* ---- solver entry points (one setup / one price vector) ---------------------------- */
-/* score_dual.hpp:64-65 dual_objective(scores, targets, prices). */
+/* score_dual.hpp:38-39 dual_objective(scores, targets, prices). */
 int rw_dual_objective(rw_ctx* ctx, const double* targets, const double* alpha, double* g);
-/* score_dual.hpp:60-61 assign_prompts(scores, prices); m_alpha must equal M. */
+/* score_dual.hpp:34 assign_prompts(scores, prices); m_alpha must equal M. */
 int rw_assign_prompts(rw_ctx* ctx, int32_t m_alpha, const double* alpha, int32_t* model_of,
                       int32_t* counts);
-/* score_dual.hpp:73-74 solve_dual(scores, targets, params); init_alpha may be NULL.
+/* score_dual.hpp:64-65 solve_dual(scores, targets, params); init_alpha may be NULL.
  * assignment (N ints) may be NULL. */
 int rw_solve_dual(rw_ctx* ctx, const double* targets, const rw_subgradient_params* params,
                   const double* init_alpha, rw_dual_solution* out, int32_t* assignment);
+/* The chosen setup's routing policy {alpha*, counts, assignment}.  PlanResult carries only
+ * w* (setup_search.hpp:53-65); the reference re-derives the policy with a cold
+ * solve_dual(scores, counts_for(w*)) (test_cli.cpp:103-106), which is optimize_fractions'
+ * canonical final solve at the winning iterate (routing_opt.cpp:121-123).  Targets are
+ * c_i = N * w_i exactly as counts_for (routing_opt.cpp:28-33).  m must equal M;
+ * assignment (N ints) may be NULL. */
+int rw_winner_policy(rw_ctx* ctx, int32_t m, const double* w_star,
+                     const rw_subgradient_params* params, rw_dual_solution* out,
+                     int32_t* assignment);
 /* routing_opt.hpp:15 project_simplex(v). Runs the device routine on one vector. */
 int rw_project_simplex(rw_ctx* ctx, int32_t m, const double* v, double* w);
-/* latency.hpp:52-77 system_latency_eval + system_latency_grad for one setup. */
+/* latency.hpp:59-77 system_latency_eval + system_latency_grad for one setup. */
 int rw_system_latency_eval(rw_ctx* ctx, const int32_t* profile_index, const double* w,
                            double lambda_rps, double kappa, double* latency_ms,
                            double* per_model_load, double* per_model_latency,
@@ -228,6 +239,12 @@ int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                        const rw_opt_context* opt, const rw_beta_params* params,
                        int32_t shard_rank, int32_t shard_count);
 int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out_records, int64_t* n_out);
+/* Let subsequent sweeps write their records into a caller-owned DEVICE buffer of
+ * cap_records records on the ctx's GPU (NULL = back to the ctx-owned buffer).  The records
+ * then never leave HBM before the cross-GPU exchange: one all-gather of these fixed-size
+ * buffers over NCCL/NVLink, e.g. torch.distributed.all_gather_into_tensor.
+ * rw_sweep_fetch still works (it reads from this buffer). */
+int rw_set_records_device(rw_ctx* ctx, void* device_records, int64_t cap_records);
 
 /* Order-deterministic winner (setup_search.cpp:246-253): feasible, max score, then min
  * latency, then smallest setup_id.  Records may come from any number of shards in any

@@ -16,6 +16,8 @@
 //   setup_search.hpp:88 select_setup       -> rw_sweep (+ host enumerate/retain, reduction)
 // Validation runs first with the reference's own validators and messages, so error
 // behaviour (ValidationError / ConfigError, errors.hpp:9-18) is the reference's.
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -220,8 +222,16 @@ BetaSearchResult optimize_beta(const SystemSetup& setup, const OptimizeContext& 
   upload(*ctx.scores);
   t.upload();
   rw_beta_result r;
-  std::vector<rw_beta_step> trace(RW_MAX_TRACE);
-  check(rw_optimize_beta(dev(), t.index.data(), &oc, &p, &r, RW_MAX_TRACE, trace.data()));
+  // every bisection step is returned, as the reference's trace holds them all: size the
+  // buffer from the bracket (the span halves each step, routing_opt.cpp:154-171)
+  double lo = params.beta_min, hi = params.beta_max;
+  if (hi < 0.0 && ctx.tau_ms > 0.0) hi = 10.0 / ctx.tau_ms;
+  double eps = params.epsilon < 0.0 ? (hi - lo) / 1024.0 : params.epsilon;
+  int cap = RW_MAX_TRACE;
+  if (hi > lo && eps > 0.0)
+    cap = std::max(cap, static_cast<int>(std::ceil(std::log2((hi - lo) / eps))) + 8);
+  std::vector<rw_beta_step> trace(cap);
+  check(rw_optimize_beta(dev(), t.index.data(), &oc, &p, &r, cap, trace.data()));
   const int m = setup.m();
   BetaSearchResult out;
   out.feasible = r.feasible != 0;
@@ -232,7 +242,7 @@ BetaSearchResult optimize_beta(const SystemSetup& setup, const OptimizeContext& 
     out.w_star = w;
   }
   if (out.feasible) out.best = relaxed(r.best, m);
-  for (int k = 0; k < r.n_trace && k < RW_MAX_TRACE; ++k)
+  for (int k = 0; k < r.n_trace && k < cap; ++k)
     out.trace.push_back({trace[k].beta, trace[k].score, trace[k].latency_ms,
                          trace[k].feasible != 0});
   return out;

@@ -74,7 +74,8 @@ class rw_setup_record(C.Structure):
                 ("tau_ms", C.c_double), ("w", C.c_double * RW_MAX_MODELS),
                 ("out_of_range", C.c_uint32),
                 ("bisect_steps", C.c_int32), ("eval_passes", C.c_int64),
-                ("polish_passes", C.c_int64), ("repair_calls", C.c_int64)]
+                ("polish_passes", C.c_int64), ("repair_calls", C.c_int64),
+                ("exec_passes", C.c_int64)]
 
 
 # numpy view of rw_setup_record (same layout) for zero-copy record arrays
@@ -82,7 +83,8 @@ RECORD_DTYPE = np.dtype([("setup_id", "<i8"), ("feasible", "<i4"), ("status", "<
                          ("score", "<f8"), ("latency_ms", "<f8"), ("beta", "<f8"),
                          ("tau_ms", "<f8"), ("w", "<f8", (RW_MAX_MODELS,)), ("out_of_range", "<u4"),
                          ("bisect_steps", "<i4"), ("eval_passes", "<i8"),
-                         ("polish_passes", "<i8"), ("repair_calls", "<i8")])
+                         ("polish_passes", "<i8"), ("repair_calls", "<i8"),
+                         ("exec_passes", "<i8")])
 assert RECORD_DTYPE.itemsize == C.sizeof(rw_setup_record)
 
 _LIB = None
@@ -113,6 +115,9 @@ def lib():
         L.rw_assign_prompts.argtypes = [C.c_void_p, C.c_int32, _dp, _ip, _ip]
         L.rw_solve_dual.argtypes = [C.c_void_p, _dp, C.POINTER(rw_subgradient_params), _dp,
                                     C.POINTER(rw_dual_solution), _ip]
+        L.rw_winner_policy.argtypes = [C.c_void_p, C.c_int32, _dp,
+                                       C.POINTER(rw_subgradient_params),
+                                       C.POINTER(rw_dual_solution), _ip]
         L.rw_project_simplex.argtypes = [C.c_void_p, C.c_int32, _dp, _dp]
         L.rw_system_latency_eval.argtypes = [C.c_void_p, _ip, _dp, C.c_double, C.c_double,
                                              _dp, _dp, _dp, _ip, _dp]
@@ -136,6 +141,7 @@ def lib():
                                          C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
                                          C.c_int32, C.c_int32]
         L.rw_sweep_fetch.argtypes = [C.c_void_p, C.c_void_p, _lp]
+        L.rw_set_records_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.rw_reduce_records.argtypes = [C.c_int64, C.c_void_p]
         L.rw_synth_scores.argtypes = [C.c_int32, C.c_int32, _dp, _dp, C.c_uint64, _dp]
         L.rw_enumerate_retain.argtypes = [C.c_int32, _ip, _ip, _ip, _ip, _dp, C.c_int32, _ip,

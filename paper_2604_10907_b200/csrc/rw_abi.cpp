@@ -42,6 +42,8 @@ struct rw_ctx {
   size_t setup_ids_cap = 0;
   rw_setup_record* d_records = nullptr;
   size_t records_cap = 0;
+  rw_setup_record* d_records_user = nullptr;  // caller-owned device buffer (optional)
+  int64_t records_user_cap = 0;
   int64_t pending_records = -1;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -75,6 +77,7 @@ std::string dstr(double x) { return std::to_string(x); }
 
 int ensure(rw_ctx* ctx, void** p, size_t* cap, size_t bytes) {
   if (*cap >= bytes && *p) return RW_OK;
+  CK(cudaSetDevice(ctx->device));  // allocations land on the ctx's GPU
   if (*p) cudaFree(*p);
   *p = nullptr;
   *cap = 0;
@@ -87,6 +90,7 @@ int ensure(rw_ctx* ctx, void** p, size_t* cap, size_t bytes) {
 int ensure_ws(rw_ctx* ctx, int slots) {
   size_t need = (size_t)slots * (size_t)ctx->n;
   if (ctx->ws_entries >= need && ctx->d_mo) return RW_OK;
+  CK(cudaSetDevice(ctx->device));
   if (ctx->d_mo) cudaFree(ctx->d_mo);
   ctx->d_mo = nullptr;
   ctx->ws_entries = 0;
@@ -104,6 +108,7 @@ int need_inputs(rw_ctx* ctx, bool profiles) {
                    "rw_b200 supports at most " + std::to_string(RW_MAX_MODELS) + " models");
   if (profiles && !ctx->d_koff)
     return set_err(ctx, RW_ERR_VALIDATION, "optimizer context: missing scores or profiles");
+  CK(cudaSetDevice(ctx->device));
   return RW_OK;
 }
 
@@ -149,6 +154,8 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
 
 // Launch + time + wait; maps device status to an error.
 int run(rw_ctx* ctx, rw::Job& j, int grid) {
+  // every launch goes to the ctx's GPU, whatever device the calling thread had current
+  CK(cudaSetDevice(ctx->device));
   j.ws_model_of = ctx->d_mo;
   CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(unsigned long long), ctx->stream));
@@ -161,6 +168,7 @@ int run(rw_ctx* ctx, rw::Job& j, int grid) {
 }
 
 int finish(rw_ctx* ctx) {
+  CK(cudaSetDevice(ctx->device));
   CK(cudaStreamSynchronize(ctx->stream));
   int32_t st = 0;
   CK(cudaMemcpy(&st, ctx->d_status, sizeof(st), cudaMemcpyDeviceToHost));
@@ -319,7 +327,7 @@ int rw_load_profiles(rw_ctx* ctx, int32_t np, const int64_t* koff, const double*
   if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
   if (np <= 0) return set_err(ctx, RW_ERR_VALIDATION, "profile table: no profiles");
   if (koff[0] != 0) return set_err(ctx, RW_ERR_VALIDATION, "profile table: offsets must start at 0");
-  for (int p = 0; p < np; ++p) {  // LatencyProfile::validate (latency.cpp:296-308)
+  for (int p = 0; p < np; ++p) {  // LatencyProfile::validate (latency.cpp:39-51)
     int64_t a = koff[p], b = koff[p + 1];
     std::string who = "profile " + std::to_string(p);
     if (b - a < 2) return set_err(ctx, RW_ERR_VALIDATION, who + ": needs at least two knots");
@@ -442,6 +450,22 @@ int rw_solve_dual(rw_ctx* ctx, const double* targets, const rw_subgradient_param
   return RW_OK;
 }
 
+int rw_winner_policy(rw_ctx* ctx, int32_t m, const double* w_star,
+                     const rw_subgradient_params* params, rw_dual_solution* out,
+                     int32_t* assignment) {
+  int rc;
+  if ((rc = need_inputs(ctx, false))) return rc;
+  if (!w_star || !params || !out)
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_winner_policy: null argument");
+  if (m != ctx->m)
+    return set_err(ctx, RW_ERR_VALIDATION,
+                   "routing fractions have " + std::to_string(m) + " entries for " +
+                       std::to_string(ctx->m) + " models");
+  std::vector<double> c(m);
+  for (int i = 0; i < m; ++i) c[i] = static_cast<double>(ctx->n) * w_star[i];  // counts_for
+  return rw_solve_dual(ctx, c.data(), params, nullptr, out, assignment);
+}
+
 int rw_project_simplex(rw_ctx* ctx, int32_t m, const double* v, double* w) {
   if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
   if (m <= 0) return set_err(ctx, RW_ERR_VALIDATION, "project_simplex: empty input");
@@ -475,7 +499,7 @@ static int upload_pidx(rw_ctx* ctx, const int32_t* pidx, size_t count) {
   return RW_OK;
 }
 
-// check_setup_and_w (latency.cpp:285-292) with RoutingFractions::validate(1e-4) (types.cpp:513)
+// check_setup_and_w (latency.cpp:28-35) with RoutingFractions::validate(1e-4) (types.cpp:88-99)
 static int validate_w(rw_ctx* ctx, int m, const double* w) {
   double tol = 1e-4, sum = 0.0;
   for (int i = 0; i < m; ++i) {
@@ -634,8 +658,11 @@ int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
   }
   const int64_t inst = n_setups * (int64_t)n_slo;
   const int64_t items = inst > shard_rank ? (inst - shard_rank + shard_count - 1) / shard_count : 0;
-  ctx->pending_records = items;
-  if (items == 0) return RW_OK;
+  ctx->pending_records = -1;  // set only once the launch below succeeded
+  if (items == 0) {
+    ctx->pending_records = 0;
+    return RW_OK;
+  }
   CK(cudaSetDevice(ctx->device));
   if ((rc = upload_pidx(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
   {
@@ -661,7 +688,13 @@ int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                        sizeof(rw_beta_params) * n_slo, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));  // `ids` is stack-owned
   }
-  {
+  if (ctx->d_records_user) {
+    if (ctx->records_user_cap < items)
+      return set_err(ctx, RW_ERR_VALIDATION,
+                     "rw_sweep: device record buffer holds " +
+                         std::to_string(ctx->records_user_cap) + " records, need " +
+                         std::to_string(items));
+  } else {
     void* p = ctx->d_records;
     size_t cap = ctx->records_cap;
     if ((rc = ensure(ctx, &p, &cap, sizeof(rw_setup_record) * items))) return rc;
@@ -681,8 +714,10 @@ int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
   j.shard_count = shard_count;
   j.opt = *opt;
   j.bp = *params;
-  j.records = ctx->d_records;
-  return run(ctx, j, grid);
+  j.records = ctx->d_records_user ? ctx->d_records_user : ctx->d_records;
+  if ((rc = run(ctx, j, grid))) return rc;
+  ctx->pending_records = items;
+  return RW_OK;
 }
 
 int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
@@ -697,6 +732,16 @@ int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                             shard_rank, shard_count);
 }
 
+int rw_set_records_device(rw_ctx* ctx, void* dev, int64_t cap) {
+  if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
+  if (dev && cap < 1) return set_err(ctx, RW_ERR_VALIDATION, "rw_set_records_device: bad capacity");
+  if (dev && (reinterpret_cast<uintptr_t>(dev) & 7u))
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_set_records_device: buffer must be 8-byte aligned");
+  ctx->d_records_user = static_cast<rw_setup_record*>(dev);
+  ctx->records_user_cap = dev ? cap : 0;
+  return RW_OK;
+}
+
 int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out, int64_t* n_out) {
   if (!ctx) return set_err(nullptr, RW_ERR_VALIDATION, "null context");
   if (ctx->pending_records < 0) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep_fetch: no sweep");
@@ -708,14 +753,16 @@ int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out, int64_t* n_out) {
   if (rc) {
     // per-record status names the first failing setup
     std::vector<rw_setup_record> recs(items);
-    cudaMemcpy(recs.data(), ctx->d_records, sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost);
+    cudaMemcpy(recs.data(), ctx->d_records_user ? ctx->d_records_user : ctx->d_records,
+               sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost);
     for (const auto& r : recs)
       if (r.status)
         return set_err(ctx, r.status, "setup " + std::to_string(r.setup_id) + ": " + ctx->err);
     return rc;
   }
   if (out)
-    CK(cudaMemcpy(out, ctx->d_records, sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out, ctx->d_records_user ? ctx->d_records_user : ctx->d_records,
+                  sizeof(rw_setup_record) * items, cudaMemcpyDeviceToHost));
   return RW_OK;
 }
 

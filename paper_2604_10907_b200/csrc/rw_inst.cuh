@@ -9,13 +9,16 @@
   namespace rw {                                                                              \
   int launch_m##MM(const Job& job, int grid, cudaStream_t st) {                               \
     using SM = Smem<MM, L, T>;                                                                \
-    static bool configured = false;                                                           \
-    if (!configured) {                                                                        \
+    /* the smem opt-in is per device: remember it per device ordinal */                      \
+    static bool configured[64] = {};                                                          \
+    int dev = 0;                                                                              \
+    cudaGetDevice(&dev);                                                                      \
+    if (dev < 0 || dev >= 64 || !configured[dev]) {                                           \
       cudaError_t e = cudaFuncSetAttribute(solver_kernel<MM, L, T>,                          \
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                                            (int)sizeof(SM));                                  \
       if (e != cudaSuccess) return (int)e;                                                    \
-      configured = true;                                                                      \
+      if (dev >= 0 && dev < 64) configured[dev] = true;                                       \
     }                                                                                         \
     solver_kernel<MM, L, T><<<grid, T, sizeof(SM), st>>>(job);                                \
     return (int)cudaGetLastError();                                                           \

@@ -208,7 +208,7 @@ class SystemSetup:
     def m(self):
         return len(self.per_model)
 
-    def validate(self):  # types.cpp:452-463
+    def validate(self):  # types.cpp:27-38
         if not self.per_model:
             raise ValidationError("setup: no models")
         seen = set()
@@ -521,6 +521,25 @@ class Engine:
             converged=bool(out.converged), counts=list(out.counts[:m]),
             eval_passes=out.eval_passes)
 
+    def winner_policy(self, w_star, params: SubgradientParams = SubgradientParams(),
+                      want_assignment=True):
+        """The chosen setup's routing policy: cold solve_dual(N * w*) (test_cli.cpp:103-106)
+        -> (DualSolution with counts, assignment as an int32 array)."""
+        w = np.ascontiguousarray(w_star, np.float64)
+        out = _abi.rw_dual_solution()
+        asg = np.zeros(self.n, np.int32) if want_assignment else None
+        p = params.c()
+        self._chk(self.L.rw_winner_policy(self.h, len(w), dptr(w), C.byref(p), C.byref(out),
+                                          iptr(asg)))
+        m = self.m
+        ds = DualSolution(
+            alpha_star=DualPrices(list(out.alpha_star[:m])), score=out.score,
+            dual_bound=out.dual_bound, duality_gap=out.duality_gap, assignment=[],
+            count_residual=list(out.count_residual[:m]), iterations=out.iterations,
+            converged=bool(out.converged), counts=list(out.counts[:m]),
+            eval_passes=out.eval_passes)
+        return ds, asg
+
     def project_simplex(self, v) -> np.ndarray:
         v = np.ascontiguousarray(v, np.float64)
         w = np.zeros(max(len(v), 1))
@@ -603,6 +622,11 @@ class Engine:
         oc = opt.c()
         self._chk(self.L.rw_sweep_slo_async(self.h, S, lptr(ids), iptr(pi), len(t), dptr(t),
                                             C.byref(oc), bps, shard_rank, shard_count))
+
+    def set_records_device(self, ptr: int, cap_records: int):
+        """Sweeps write their records into this caller-owned device buffer (0 = ctx-owned)."""
+        self._chk(self.L.rw_set_records_device(self.h, C.c_void_p(ptr or None),
+                                               int(cap_records)))
 
     def sweep_fetch(self):
         _, _, _, S, r, cnt = self._pending
@@ -739,7 +763,7 @@ def _check_context(setup: SystemSetup, ctx: OptimizeContext):
 
 def system_latency_eval(lib: ProfileLibrary, setup: SystemSetup, w: RoutingFractions,
                         lambda_rps: float, metric: Metric, kappa: float):
-    """latency.cpp:443-461 (+ grad, :429-441), evaluated on device."""
+    """latency.cpp:186-204 (+ grad, :429-441), evaluated on device."""
     if w.m() != setup.m():
         raise ValidationError(f"routing fractions have {w.m()} entries for {setup.m()} models")
     b = _ProfileTableBuilder(lib, metric)
@@ -822,7 +846,7 @@ def enumerate_retain(space: SetupSpace, gpu_count: int, rho_floor: float, mem: M
         iptr(mm), iptr(mt), dptr(mf), gpu_count, rho_floor, total, C.byref(n_enum),
         iptr(verdict), iptr(tp_out), dptr(rho_out))
     if rc == _abi.RW_ERR_CONFIG:
-        # name the first missing (model, tp) like MemoryTable::at (types.cpp:482-490)
+        # name the first missing (model, tp) like MemoryTable::at (types.cpp:57-65)
         for i, name in enumerate(space.models):
             for tp in space.tp_choices[i]:
                 mem.at(name, tp)

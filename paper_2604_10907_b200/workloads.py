@@ -91,8 +91,13 @@ def config(name: str, n: Optional[int] = None) -> SweepConfig:
     return c
 
 
-def scores_for(cfg: SweepConfig) -> np.ndarray:
-    s = rp.synth_scores(cfg.n, cfg.models, beta_shapes(cfg.m), cfg.seed).scores
+def scores_for(cfg: SweepConfig, synth=None) -> np.ndarray:
+    """synth(n, shapes, seed) -> matrix overrides the host producer (the bench's reference
+    arm passes the reference library's own synth_scores, so it loads nothing of ours)."""
+    if synth is None:
+        s = rp.synth_scores(cfg.n, cfg.models, beta_shapes(cfg.m), cfg.seed).scores
+    else:
+        s = synth(cfg.n, beta_shapes(cfg.m), cfg.seed)
     if cfg.ties:
         s = tie_scores(s, cfg.seed)
     return s
@@ -131,13 +136,29 @@ class SweepInputs:
     enumerated: int
 
 
-def build_inputs(cfg: SweepConfig, limit: Optional[int] = None) -> SweepInputs:
+class _SpaceView:
+    """The plain setup-space description an external enumerate/retain takes."""
+
+    def __init__(self, cfg: SweepConfig):
+        self.tp_choices = [list(t) for t in cfg.tp_choices]
+        self.rho_choices = [list(r) for r in cfg.rho_choices]
+        self.memory = [(cfg.models.index(mdl), tp, f) for (mdl, tp), f in cfg.mem.items()]
+        self.gpu_count, self.rho_floor = cfg.gpu_count, cfg.rho_floor
+
+
+def build_inputs(cfg: SweepConfig, limit: Optional[int] = None,
+                 enumerate_fn=None) -> SweepInputs:
+    """enumerate_fn(space_view) -> (verdict, tp, rho) overrides the host enumerate/retain
+    (the bench's reference arm passes the reference library's own)."""
     space = rp.SetupSpace(list(cfg.models), [list(t) for t in cfg.tp_choices],
                           [list(r) for r in cfg.rho_choices])
     mem = rp.MemoryTable()
     for (mdl, tp), f in cfg.mem.items():
         mem.insert(mdl, tp, f)
-    verdict, tps, rhos = rp.enumerate_retain(space, cfg.gpu_count, cfg.rho_floor, mem)
+    if enumerate_fn is None:
+        verdict, tps, rhos = rp.enumerate_retain(space, cfg.gpu_count, cfg.rho_floor, mem)
+    else:
+        verdict, tps, rhos = enumerate_fn(_SpaceView(cfg))
     retained = np.nonzero(verdict == 0)[0]
     if limit is not None:
         retained = retained[:limit]

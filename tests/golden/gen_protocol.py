@@ -1,0 +1,174 @@
+#!/usr/bin/env python3
+"""Generates tests/golden/protocol_*.json: BASELINE.md's parity protocol run through the
+UNMODIFIED reference library (oracle/_ref/libroutewise_ref.so, compiled from
+/root/reference/proj/src by oracle/Makefile) in this container.  TEST INFRASTRUCTURE ONLY.
+
+Protocol (BASELINE.md "CPU-baseline plan" step 4): full N, the first 64 retained setups,
+the truncated schedule (subgradient 20, PGA 5, beta epsilon = span/4); C2 at all 8 SLOs;
+plus one default-schedule sweep (C1 shape at reduced N, all 64 setups, config.hpp:20-31).
+
+The "first 64 retained setups" of a config are a restricted setup space: enumeration is
+model-major with model 0 the most significant digit (setup_search.cpp:99-125), so fixing
+the leading models to their first choice and keeping the trailing models' full choice lists
+enumerates exactly the first S setups of the full space, in the same order and with the
+same ordinals (the fixed digits are 0).  Every setup of these configs is retained.
+
+Per config the fixture holds:
+  * the reference select_setup sweep rows (setup_search.cpp:187-253): id, feasible,
+    score / latency bits, and the plan (winner id, w*, beta*, score, latency);
+  * per setup, the C restatement's full record (beta, w, eval/polish/repair counts) — the
+    restatement is pinned to the reference (tests/test_oracle_pin.py), the reference API
+    does not expose them;
+  * the winner's routing policy: the reference solve_dual(N * w*) (test_cli.cpp:103-106)
+    -> alpha*, score, counts and a SHA-256 of the assignment;
+  * a SHA-256 of the score matrix, so the GPU test proves it ran on identical inputs.
+
+Usage: python tests/golden/gen_protocol.py [C2 C3 C5 C1D ...]   (minutes each, 8 threads)
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import time
+from multiprocessing import Pool
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from paper_2604_10907_b200 import workloads as wl  # noqa: E402  (host input producers)
+from oracle import Oracle, Params, ProfileTable, Reference  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+# name -> (config, n override, leading models fixed to their first choice, schedule)
+SPECS = {
+    "C2": ("C2", None, 1, "truncated"),
+    "C3": ("C3", None, 3, "truncated"),
+    "C5": ("C5", None, 2, "truncated"),
+    "C1D": ("C1", 2000, 0, "default"),
+}
+
+
+def hx(x):
+    return float(x).hex()
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def params_for(schedule, tau):
+    if schedule == "default":
+        return Params()
+    hi = 10.0 / tau
+    return Params(sub_max_iters=20, pga_max_iters=5, epsilon=hi / 4.0)
+
+
+class Space:
+    pass
+
+
+def restricted_space(cfg, inp, fixed, tau):
+    sp = Space()
+    sp.tp_choices = [[t[0]] if i < fixed else list(t) for i, t in enumerate(cfg.tp_choices)]
+    sp.rho_choices = [[r[0]] if i < fixed else list(r) for i, r in enumerate(cfg.rho_choices)]
+    sp.memory = [(cfg.models.index(mdl), tp, f) for (mdl, tp), f in cfg.mem.items()]
+    sp.profile_keys = inp.profile_keys
+    sp.profiles = ProfileTable(inp.koff, inp.kx, inp.ky)
+    sp.gpu_count, sp.rho_floor = cfg.gpu_count, cfg.rho_floor
+    sp.lambda_rps, sp.tau_ms, sp.kappa = cfg.lambda_rps, tau, cfg.kappa
+    return sp
+
+
+_G = {}
+
+
+def _init(name):
+    cfg_name, n, _, _ = SPECS[name]
+    cfg = wl.config(cfg_name, n)
+    _G["cfg"] = cfg
+    _G["inp"] = wl.build_inputs(cfg)
+    _G["s"] = wl.scores_for(cfg)
+    _G["o"] = Oracle()
+
+
+def _oracle_record(args):
+    k, tau, schedule = args
+    cfg, inp, s, o = _G["cfg"], _G["inp"], _G["s"], _G["o"]
+    p = params_for(schedule, tau)
+    prof = ProfileTable(inp.koff, inp.kx, inp.ky)
+    r = o.evaluate_setup(s, prof, inp.profile_index[k], cfg.lambda_rps, tau, cfg.kappa, p)
+    return dict(k=k, tau=tau, feasible=bool(r["feasible"]), score=hx(r["score"]),
+                latency_ms=hx(r["latency_ms"]), beta=hx(r["beta"]),
+                w=[hx(x) for x in r["w"]], eval_passes=int(r["eval_passes"]),
+                polish_passes=int(r["polish_passes"]), repair_calls=int(r["repair_calls"]))
+
+
+def generate(name, threads):
+    cfg_name, n, fixed, schedule = SPECS[name]
+    cfg = wl.config(cfg_name, n)
+    inp = wl.build_inputs(cfg)
+    s = wl.scores_for(cfg)
+    R = Reference()
+    out = dict(config=cfg_name, n=cfg.n, m=cfg.m, schedule=schedule, fixed_models=fixed,
+               scores_sha256=sha(s), generator="tests/golden/gen_protocol.py",
+               reference="oracle/_ref/libroutewise_ref.so (unmodified /root/reference sources)",
+               slos=[])
+    for tau in cfg.taus:
+        p = params_for(schedule, tau)
+        sp = restricted_space(cfg, inp, fixed, tau)
+        t0 = time.time()
+        ref = R.select_setup(s, sp, p, parallelism=threads)
+        dt = time.time() - t0
+        S = ref["retained"]
+        assert S == ref["enumerated"], "every setup of the sample must be retained"
+        ids = [int(x) for x in ref["sweep_id"]]
+        assert ids == list(range(S)) and np.array_equal(inp.retained[:S], np.arange(S))
+        # the winner's routing policy (test_cli.cpp:103-106: solve_dual(N * w*))
+        pol = None
+        if ref["feasible"]:
+            c = cfg.n * ref["w"]
+            d = R.solve_dual(s, c, Params(eta0=p.eta0, sub_max_iters=p.sub_max_iters,
+                                          residual_tol=p.residual_tol,
+                                          polish_passes=p.polish_passes))
+            counts = np.bincount(d["assignment"], minlength=cfg.m).astype(np.int64)
+            pol = dict(alpha=[hx(x) for x in d["alpha"]], score=hx(d["score"]),
+                       dual_bound=hx(d["dual_bound"]), counts=[int(x) for x in counts],
+                       assignment_sha256=sha(d["assignment"].astype(np.int32)))
+        with Pool(threads, initializer=_init, initargs=(name,)) as pool:
+            orc = pool.map(_oracle_record, [(k, tau, schedule) for k in range(S)])
+        win = None
+        for k in range(S):  # the plan's setup among the sweep rows
+            if ref["feasible"] and hx(ref["sweep_score"][k]) == hx(ref["score"]) and \
+                    hx(ref["sweep_latency"][k]) == hx(ref["latency_ms"]) and \
+                    bool(ref["sweep_feasible"][k]):
+                win = k
+                break
+        out["slos"].append(dict(
+            tau=tau, params=dict(sub_max_iters=p.sub_max_iters, pga_max_iters=p.pga_max_iters,
+                                 epsilon=hx(p.epsilon)),
+            ref_seconds=dt, threads=threads, setups=S,
+            sweep=[dict(id=ids[k], feasible=bool(ref["sweep_feasible"][k]),
+                        score=hx(ref["sweep_score"][k]), latency_ms=hx(ref["sweep_latency"][k]))
+                   for k in range(S)],
+            plan=dict(feasible=bool(ref["feasible"]), winner=win, score=hx(ref["score"]),
+                      latency_ms=hx(ref["latency_ms"]), beta=hx(ref["beta"]),
+                      w=[hx(x) for x in ref["w"]]),
+            policy=pol, oracle=orc))
+        print(f"{name} tau={tau}: {S} setups, reference {dt:.1f}s, winner {win}", flush=True)
+    path = os.path.join(OUT, f"protocol_{name}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0)
+    print("wrote", path, flush=True)
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(SPECS)
+    threads = os.cpu_count() or 1
+    for nm in names:
+        generate(nm, threads)

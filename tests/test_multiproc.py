@@ -65,7 +65,7 @@ def _worker(rank, world, port, q):
         n_inst = len(inp.retained) * len(taus)
         ids = shard.shard_of(n_inst, rank, world)
         mine = _records(ids, cfg, inp, s, prof, taus, p)
-        allrec = shard.gather_records(mine)
+        allrec = shard.gather_records(mine, n_inst)
         win = shard.winners_per_slo(allrec, taus)
         if rank == 0:
             q.put((allrec.tobytes(), {t: int(allrec[i]["setup_id"]) if i >= 0 else -1

@@ -22,17 +22,21 @@ eng.set_profiling(True)
 recs = eng.sweep(inp.profile_index, inp.retained, opt, bp)
 ms = eng.last_kernel_ms()
 pr = eng.profile()
-p = int(recs["eval_passes"].sum()); pp = int(recs["polish_passes"].sum())
+p = int(recs["exec_passes"].sum()); pp = int(recs["polish_passes"].sum())
+pref = int(recs["eval_passes"].sum())
 ctas = min(len(recs), 296)
 cyc = ms * 1.965e6
 names = ["load(w0)", "totbar(w0)", "empty(w0)", "polish", "pmiss", "pradix", "walk_wait",
          "walk_busy", "fast_blocks", "slow_blocks", "raw_rows", "psweep", "pselect", "pass",
-         "repair", "p1_rounds", "p2_passes", "moves"]
+         "repair", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell", "p_move"]
 print(f"{which} x{len(recs)} ({sched}): kernel {ms:.3f} ms (~{cyc:.3e} cyc/CTA), eval passes {p}, "
-      f"polish passes {pp}, evals/s {p * cfg.n / (ms / 1e3):.3e}")
+      f"(reference trajectory {pref}), polish passes {pp}, evals/s {p * cfg.n / (ms / 1e3):.3e}")
 for i, nm in enumerate(names):
     v = pr[i]
-    if nm in ("pmiss", "pradix", "fast_blocks", "slow_blocks", "raw_rows", "p1_rounds", "p2_passes", "moves"):
+    if nm in ("pmiss", "pradix", "fast_blocks", "slow_blocks", "raw_rows", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell"):
         print(f"  {nm:12s} {v:14d}  per pass {v / max(p, 1):10.2f}")
+    elif nm == "p_move":
+        ncoord = max(pp * cfg.m, 1)
+        print(f"  {nm:12s} mean log2(|move|/d) over nonzero moves ~ {v / ncoord - 64:8.2f} (all coords {ncoord})")
     elif nm != "-":
         print(f"  {nm:12s} {v / ctas:14.3e} cyc/CTA  {100.0 * v / ctas / cyc:5.1f}%  per pass {v / max(p, 1):10.0f}")
