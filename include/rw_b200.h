@@ -147,6 +147,8 @@ typedef struct {
 
 /* ---- lifecycle ------------------------------------------------------------------- */
 int rw_abi_version(void);
+/* CUDA devices visible to this process (0 when none). */
+int rw_device_count(void);
 int rw_create(int device, rw_ctx** out);
 void rw_destroy(rw_ctx* ctx);
 /* Last error message of ctx (or of the calling thread when ctx is NULL). */
@@ -245,6 +247,19 @@ int rw_sweep_fetch(rw_ctx* ctx, rw_setup_record* out_records, int64_t* n_out);
  * buffers over NCCL/NVLink, e.g. torch.distributed.all_gather_into_tensor.
  * rw_sweep_fetch still works (it reads from this buffer). */
 int rw_set_records_device(rw_ctx* ctx, void* device_records, int64_t cap_records);
+
+/* select_setup's per-setup half over several GPUs (SearchParams::parallelism,
+ * setup_search.hpp:74-77, mapped to GPUs): one host thread per context, shard r of W =
+ * n_ctx solved on ctxs[r] (instances k with k % W == r), each context
+ * holding its own replica of the scores and profiles.  The fixed-size records come back
+ * in instance order (k = slo * n_setups + setup), so the result is bit-identical to a
+ * single-GPU rw_sweep_slo; out_records holds n_setups * n_slo records.  Errors: the first
+ * failing shard in rank order (the reference rethrows worker failures in thread order,
+ * setup_search.cpp:230-235); its message is set on ctxs[0]. */
+int rw_sweep_multi(rw_ctx* const* ctxs, int32_t n_ctx, int64_t n_setups,
+                   const int64_t* setup_ids, const int32_t* profile_index, int32_t n_slo,
+                   const double* tau_ms, const rw_opt_context* opt,
+                   const rw_beta_params* params, rw_setup_record* out_records);
 
 /* Order-deterministic winner (setup_search.cpp:246-253): feasible, max score, then min
  * latency, then smallest setup_id.  Records may come from any number of shards in any

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -48,6 +49,22 @@ rw_ctx* dev() {
   return ctx;
 }
 
+// Contexts of shards 1.. of a multi-GPU select_setup: shard r lives on device r % #GPUs.
+// (RW_SHIM_SHARED_GPU=1 lets more shards than GPUs share devices — a test hook that runs
+// the multi-shard path on one GPU.)
+rw_ctx* shard_ctx(int r) {
+  static std::vector<rw_ctx*> ctxs;
+  if (r == 0) return dev();
+  while (static_cast<int>(ctxs.size()) < r) ctxs.push_back(nullptr);
+  rw_ctx*& c = ctxs[r - 1];
+  if (!c) {
+    const int ndev = std::max(1, rw_device_count());
+    if (rw_create(r % ndev, &c) != RW_OK)
+      throw std::runtime_error(std::string("rw_create: ") + rw_last_error(nullptr));
+  }
+  return c;
+}
+
 void check(int rc) {
   if (rc == RW_OK) return;
   const std::string msg = rw_last_error(dev());
@@ -56,8 +73,8 @@ void check(int rc) {
   throw std::runtime_error("rw_b200: " + msg);
 }
 
-void upload(const ScoreMatrix& s) {
-  check(rw_load_scores(dev(), s.n(), s.m(), s.scores.data()));
+void upload(const ScoreMatrix& s, rw_ctx* c = nullptr) {
+  check(rw_load_scores(c ? c : dev(), s.n(), s.m(), s.scores.data()));
 }
 
 void check_dims(const ScoreMatrix& scores, const TargetCounts& targets) {  // score_dual.cpp:15
@@ -107,9 +124,9 @@ struct ProfileTable {
       index.push_back(it->second);
     }
   }
-  void upload() const {
-    check(rw_load_profiles(dev(), static_cast<int32_t>(koff.size() - 1), koff.data(), kx.data(),
-                           ky.data()));
+  void upload(rw_ctx* c = nullptr) const {
+    check(rw_load_profiles(c ? c : dev(), static_cast<int32_t>(koff.size() - 1), koff.data(),
+                           kx.data(), ky.data()));
   }
 };
 
@@ -280,13 +297,32 @@ SearchOutput select_setup(const SetupSpace& space, const SearchContext& ctx,
   rw_beta_params p = beta_params(params.beta);
   rw_opt_context oc{ctx.opt.lambda_rps, ctx.opt.tau_ms, ctx.opt.kappa};
   std::vector<rw_setup_record> recs(retained_ids.size());
-  int64_t n_out = 0;
+  int64_t n_out = static_cast<int64_t>(retained_ids.size());
+  // SearchParams::parallelism (setup_search.cpp:213-215: worker threads, <= 0 -> all) maps
+  // to GPUs: shard r of W on GPU r, one host thread each, records gathered in setup order
+  const int ndev = std::max(1, rw_device_count());
+  const char* shared = std::getenv("RW_SHIM_SHARED_GPU");
+  int shards = params.parallelism > 0 ? params.parallelism : ndev;
+  if (!(shared && shared[0] == '1')) shards = std::min(shards, ndev);
+  shards = std::clamp<int>(shards, 1, static_cast<int>(retained_ids.size()));
   {
     std::lock_guard<std::mutex> lk(g_mu);
-    upload(*ctx.opt.scores);
-    t.upload();
-    check(rw_sweep(dev(), static_cast<int64_t>(retained_ids.size()), retained_ids.data(),
-                   t.index.data(), &oc, &p, 0, 1, recs.data(), &n_out));
+    if (shards == 1) {
+      upload(*ctx.opt.scores);
+      t.upload();
+      check(rw_sweep(dev(), static_cast<int64_t>(retained_ids.size()), retained_ids.data(),
+                     t.index.data(), &oc, &p, 0, 1, recs.data(), &n_out));
+    } else {
+      std::vector<rw_ctx*> cs(shards);
+      for (int r = 0; r < shards; ++r) {
+        cs[r] = shard_ctx(r);
+        upload(*ctx.opt.scores, cs[r]);
+        t.upload(cs[r]);
+      }
+      const double tau = oc.tau_ms;
+      check(rw_sweep_multi(cs.data(), shards, static_cast<int64_t>(retained_ids.size()),
+                           retained_ids.data(), t.index.data(), 1, &tau, &oc, &p, recs.data()));
+    }
   }
   out.sweep.reserve(retained_ids.size());
   for (size_t k = 0; k < retained_ids.size(); ++k)  // records come back in enumeration order

@@ -1,5 +1,7 @@
 // rw_abi.cpp — the C-ABI (include/rw_b200.h): context, input upload, validation with the
 // reference's error texts, job launch and result download.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -7,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rw_b200.h"
@@ -21,6 +24,8 @@ struct rw_ctx {
   double* d_scores_owned = nullptr;
   size_t scores_cap = 0;  // doubles
   int32_t n = 0, m = 0;
+  CUtensorMap tmap;        // 2-D TMA descriptor of the scores (swizzled_m(m) only)
+  bool tmap_ok = false;
   // profiles
   int64_t* d_koff = nullptr;
   double* d_kx = nullptr;
@@ -30,6 +35,8 @@ struct rw_ctx {
   // workspace
   uint8_t* d_mo = nullptr;
   size_t ws_entries = 0;  // slots * n capacity
+  unsigned char* d_ph2 = nullptr;  // repair Phase-2 lists, slots * ph2_stride(m)
+  size_t ph2_bytes = 0;
   // generic io
   void* d_io = nullptr;
   size_t io_cap = 0;
@@ -72,6 +79,44 @@ int cuda_err(rw_ctx* ctx, cudaError_t e, const char* where) {
     if (e_ != cudaSuccess) return cuda_err(ctx, e_, #call);   \
   } while (0)
 
+// The driver's tensor-map encoder, fetched through the runtime (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// (Re)build the score matrix's tensor map: dims {M, N} doubles, row pitch 8M bytes, box
+// {M, SR} = one ring stage, smem swizzle = the row width (32/64/128 B), zero fill past N.
+int encode_scores_map(rw_ctx* ctx) {
+  ctx->tmap_ok = false;
+  if (!rw::swizzled_m(ctx->m)) return RW_OK;
+  auto enc = tensor_map_encoder();
+  if (!enc) return set_err(ctx, RW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)ctx->m, (cuuint64_t)ctx->n};
+  const cuuint64_t strides[1] = {(cuuint64_t)ctx->m * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)ctx->m, (cuuint32_t)rw::stage_rows(ctx->m)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle swz = ctx->m == 4 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : ctx->m == 8 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                               : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = enc(&ctx->tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                   const_cast<double*>(ctx->d_scores), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(ctx, RW_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  ctx->tmap_ok = true;
+  return RW_OK;
+}
+
 // libstdc++'s std::to_string(double) (the reference builds its messages with it).
 std::string dstr(double x) { return std::to_string(x); }
 
@@ -89,6 +134,15 @@ int ensure(rw_ctx* ctx, void** p, size_t* cap, size_t bytes) {
 
 int ensure_ws(rw_ctx* ctx, int slots) {
   size_t need = (size_t)slots * (size_t)ctx->n;
+  const size_t ph2 = (size_t)slots * (size_t)rw::ph2_stride(ctx->m > 0 ? ctx->m : 1);
+  if (ctx->ph2_bytes < ph2 || !ctx->d_ph2) {
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->d_ph2) cudaFree(ctx->d_ph2);
+    ctx->d_ph2 = nullptr;
+    ctx->ph2_bytes = 0;
+    CK(cudaMalloc(&ctx->d_ph2, ph2));
+    ctx->ph2_bytes = ph2;
+  }
   if (ctx->ws_entries >= need && ctx->d_mo) return RW_OK;
   CK(cudaSetDevice(ctx->device));
   if (ctx->d_mo) cudaFree(ctx->d_mo);
@@ -138,6 +192,8 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
   rw::Job j;
   std::memset(&j, 0, sizeof(j));
   j.kind = kind;
+  j.tmap = ctx->tmap;
+  j.tmap_ok = ctx->tmap_ok ? 1 : 0;
   j.n = ctx->n;
   j.m = ctx->m;
   j.scores = ctx->d_scores;
@@ -146,6 +202,10 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
   j.ky = ctx->d_ky;
   j.shard_count = 1;
   j.ws_model_of = ctx->d_mo;
+  j.ws_ph2 = ctx->d_ph2;
+  j.ph2_stride = rw::ph2_stride(ctx->m > 0 ? ctx->m : 1);
+  j.ph2_k = rw::ph2_k(ctx->m > 0 ? ctx->m : 1);
+  j.ph2_ec = rw::ph2_ec(ctx->m);
   j.queue = ctx->d_queue;
   j.status_out = ctx->d_status;
   j.prof_out = ctx->d_prof;
@@ -156,7 +216,10 @@ rw::Job base_job(rw_ctx* ctx, int kind) {
 int run(rw_ctx* ctx, rw::Job& j, int grid) {
   // every launch goes to the ctx's GPU, whatever device the calling thread had current
   CK(cudaSetDevice(ctx->device));
+  if (rw::swizzled_m(j.m) && j.n > 0 && !j.tmap_ok)  // the kernel has no other load path
+    return set_err(ctx, RW_ERR_CUDA, "score tensor map missing");
   j.ws_model_of = ctx->d_mo;
+  j.ws_ph2 = ctx->d_ph2;
   CK(cudaMemsetAsync(ctx->d_status, 0, sizeof(int32_t), ctx->stream));
   CK(cudaMemsetAsync(ctx->d_queue, 0, sizeof(unsigned long long), ctx->stream));
   CK(cudaEventRecord(ctx->ev0, ctx->stream));
@@ -184,6 +247,12 @@ int finish(rw_ctx* ctx) {
 extern "C" {
 
 int rw_abi_version(void) { return RW_ABI_VERSION; }
+
+int rw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
 
 int rw_create(int device, rw_ctx** out) {
   if (!out) return set_err(nullptr, RW_ERR_VALIDATION, "rw_create: null out");
@@ -222,6 +291,7 @@ void rw_destroy(rw_ctx* ctx) {
   cudaFree(ctx->d_kx);
   cudaFree(ctx->d_ky);
   cudaFree(ctx->d_mo);
+  cudaFree(ctx->d_ph2);
   cudaFree(ctx->d_io);
   cudaFree(ctx->d_queue);
   cudaFree(ctx->d_status);
@@ -305,7 +375,7 @@ int rw_load_scores(rw_ctx* ctx, int32_t n, int32_t m, const double* host) {
   ctx->d_scores = ctx->d_scores_owned;
   ctx->n = n;
   ctx->m = m;
-  return RW_OK;
+  return encode_scores_map(ctx);
 }
 
 int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* dev) {
@@ -319,7 +389,7 @@ int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* dev) 
   ctx->d_scores = dev;
   ctx->n = n;
   ctx->m = m;
-  return RW_OK;
+  return encode_scores_map(ctx);
 }
 
 int rw_load_profiles(rw_ctx* ctx, int32_t np, const int64_t* koff, const double* kx,
@@ -774,6 +844,45 @@ int rw_sweep_slo(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const 
                               shard_rank, shard_count);
   if (rc) return rc;
   return rw_sweep_fetch(ctx, out, n_out);
+}
+
+int rw_sweep_multi(rw_ctx* const* ctxs, int32_t n_ctx, int64_t n_setups,
+                   const int64_t* setup_ids, const int32_t* pidx, int32_t n_slo,
+                   const double* taus, const rw_opt_context* opt, const rw_beta_params* params,
+                   rw_setup_record* out) {
+  if (!ctxs || n_ctx < 1 || !ctxs[0])
+    return set_err(nullptr, RW_ERR_VALIDATION, "rw_sweep_multi: no contexts");
+  for (int r = 0; r < n_ctx; ++r)
+    if (!ctxs[r]) return set_err(ctxs[0], RW_ERR_VALIDATION, "rw_sweep_multi: null context");
+  if (n_setups < 0 || n_slo < 1)
+    return set_err(ctxs[0], RW_ERR_VALIDATION, "rw_sweep: bad setup / SLO count");
+  const int64_t inst = n_setups * (int64_t)n_slo;
+  std::vector<std::vector<rw_setup_record>> part(n_ctx);
+  std::vector<int> rc(n_ctx, RW_OK);
+  std::vector<int64_t> got(n_ctx, 0);
+  // one host thread drives each GPU (its context owns a stream and device buffers)
+  auto shard = [&](int r) {
+    const int64_t items = inst > r ? (inst - r + n_ctx - 1) / n_ctx : 0;
+    part[r].resize(std::max<int64_t>(items, 1));
+    rc[r] = rw_sweep_slo(ctxs[r], n_setups, setup_ids, pidx, n_slo, taus, opt, params, r,
+                         n_ctx, part[r].data(), &got[r]);
+  };
+  if (n_ctx == 1) {
+    shard(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int r = 0; r < n_ctx; ++r) pool.emplace_back(shard, r);
+    for (auto& t : pool) t.join();
+  }
+  for (int r = 0; r < n_ctx; ++r)
+    if (rc[r] != RW_OK) {
+      if (r != 0) ctxs[0]->err = "shard " + std::to_string(r) + ": " + ctxs[r]->err;
+      return rc[r];
+    }
+  // the combine: interleaved shards back into instance order
+  for (int r = 0; r < n_ctx; ++r)
+    for (int64_t i = 0; i < got[r]; ++i) out[r + i * n_ctx] = part[r][i];
+  return RW_OK;
 }
 
 int rw_sweep(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const int32_t* pidx,

@@ -1,6 +1,7 @@
 // Job descriptor shared by the host ABI (rw_abi.cpp) and the device solver (rw_solver.cuh).
 // Passed by value as the kernel parameter; every pointer is device memory.
 #pragma once
+#include <cuda.h>  // CUtensorMap (header only; the encoder is fetched through the runtime)
 #include <stdint.h>
 
 #include "rw_b200.h"
@@ -19,6 +20,11 @@ enum JobKind : int32_t {
 };
 
 struct Job {
+  // 2-D tiled TMA descriptor of the score matrix (box = one ring stage of SR rows, with the
+  // 32/64/128-byte smem swizzle matching the row width), for M in {4, 8, 16}; the kernel
+  // takes the Job as a __grid_constant__ parameter so the descriptor lives in param space.
+  alignas(64) CUtensorMap tmap;
+  int32_t tmap_ok;
   int32_t kind;
   int32_t n, m;
   const double* scores;
@@ -54,9 +60,32 @@ struct Job {
   char* msg_out;        // job-level message buffer (256 bytes)
   // workspace, one slot of n entries per CTA
   uint8_t* ws_model_of;
+  // repair Phase-2 pair lists, one slot of ph2_stride bytes per CTA (Solver::ph2_ws)
+  unsigned char* ws_ph2;
+  long long ph2_stride;
+  int32_t ph2_k, ph2_ec;
   unsigned long long* queue;
   long long* prof_out;  // optional diagnostics counters [RW_PROF_SLOTS]
 };
+
+// Repair Phase-2 list geometry for m models: K best members per pair (<= the 2048-pair
+// sort buffer), EC joined rows per pair, about 1 MB per CTA slot.
+inline int ph2_ec(int m) { (void)m; return 64; }
+inline int ph2_k(int m) {
+  const long long pairs = (long long)m * m;
+  long long k = (1ll << 20) / (pairs * 12) - ph2_ec(m);
+  return (int)(k < 16 ? 16 : (k > 2048 ? 2048 : k));
+}
+inline long long ph2_stride(int m) {
+  const long long pairs = (long long)m * m;
+  long long b = pairs * (ph2_k(m) + ph2_ec(m)) * 12 + pairs * 24;
+  return (b + 255) / 256 * 256;
+}
+
+// Rows per TMA ring stage of the kernel instantiated for m models (Smem<MM,...>::SR).
+inline int stage_rows(int m) { return m <= 4 ? 128 : (m <= 8 ? 64 : 32); }
+// M for which the eval / polish streams use the swizzled tensor-map copies.
+inline bool swizzled_m(int m) { return m == 4 || m == 8 || m == 16; }
 
 // Host launcher (rw_kernels.cu). Returns a cudaError_t value.
 int launch_job(const Job& job, int grid, void* stream);

@@ -22,6 +22,9 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#ifdef RW_WATCHDOG
+#include <cstdio>
+#endif
 
 #include "rw_job.h"
 
@@ -94,6 +97,7 @@ enum Prof {
   PR_PFAR = 19,      // polish: the k-th largest was outside the outermost window
   PR_PSHELL = 20,    // polish: in a middle shell (second sweep gathers it)
   PR_PMOVE = 21,     // polish: sum over coordinates of round(log2(|move| / d)) + 64
+  PR_P2REFRESH = 22, // repair Phase 2: pair lists rebuilt
 };
 struct Piece {
   long long q;
@@ -117,12 +121,19 @@ struct Smem {
 #ifndef RW_SR4
 #define RW_SR4 128
 #endif
+  static_assert(RW_SR4 == 128, "stage_rows() in rw_job.h mirrors SR");
   static constexpr int SR = (MM <= 4) ? RW_SR4 : ((MM <= 8) ? 64 : 32);
   static constexpr int RL = SR / 32;    // rows per lane per stage
   static constexpr int STAGE_BYTES = SR * MM * 8;
   static_assert(L % RL == 0, "a block is a whole number of stages");
-  __align__(128) unsigned char ring[WP][2][STAGE_BYTES];
+  // 1024-aligned stages: the tensor-map copies swizzle on absolute smem address bits
+  __align__(1024) unsigned char ring[WP][2][STAGE_BYTES];
   unsigned long long stage_bar[WP][2];
+  // stages each producer warp has consumed since the launch: the stage barriers are
+  // initialised once per launch and their phases carried across passes and sweeps
+  // (stage g of warp w uses slot g & 1, parity (g >> 1) & 1) — re-initialising an mbarrier
+  // between sweeps stalled warps at random (round-1 note, reproduced with RW_WATCHDOG)
+  unsigned stg_cnt[WP];
   unsigned long long full_bar[2], empty_bar[2];
   double raw[2][WP][RAWW];              // RAW sub-segments' b (tile parity)
   Piece pieces[2][WP][MAXP];            // double-buffered by tile parity
@@ -284,7 +295,7 @@ enum PassMode { PASS_EVAL = 0, PASS_FIXED = 1 };
 // compiles to LDS/STS (a reference member would decay to generic LD/ST).
 template <class SMT>
 __device__ __forceinline__ SMT& smem() {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   return *reinterpret_cast<SMT*>(smem_raw);
 }
 #define SMX (smem<SM>())
@@ -347,12 +358,31 @@ struct Solver {
   }
   __device__ __forceinline__ static void mbar_wait(unsigned long long* bar, unsigned parity) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+#ifdef RW_WATCHDOG
+    // debug builds (make EXTRA=-DRW_WATCHDOG): a wait that never completes names itself
+    for (long long spin = 0;; ++spin) {
+      unsigned ok;
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+          " selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(ok)
+          : "r"(a), "r"(parity), "r"(1000000)
+          : "memory");
+      if (ok) return;
+      if (spin == (1ll << 22)) {
+        printf("RW_WATCHDOG: block %d warp %d lane %d stuck on mbarrier smem+%u parity %u\n",
+               blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, a, parity);
+        __trap();
+      }
+    }
+#else
     asm volatile(
         "{\n .reg .pred p;\n WAIT_%=:\n"
         " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         " @!p bra WAIT_%=;\n}" ::"r"(a),
         "r"(parity), "r"(0x989680)
         : "memory");
+#endif
   }
   // Warp sums evaluated in one fixed order and broadcast, so every lane holds the same bits.
   __device__ __forceinline__ static double warp_sum_d(double x) {
@@ -429,7 +459,6 @@ struct Solver {
       for (int q = 0; q < 2; ++q) {
         mbar_init(&SMX.full_bar[q], WP);
         mbar_init(&SMX.empty_bar[q], 1);
-        for (int w2 = 0; w2 < WP; ++w2) mbar_init(&SMX.stage_bar[w2][q], 1);
       }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -658,6 +687,47 @@ struct Solver {
         : "memory");
   }
 
+  // 2-D tiled TMA: SR rows x M doubles at row r0 into a stage, swizzled (see rd2).  Rows
+  // past N are zero-filled and still counted in the transaction bytes (the full box).
+  __device__ __forceinline__ void tma_load_rows(void* dst, int r0, unsigned long long* bar) const {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(d),
+        "l"(reinterpret_cast<unsigned long long>(&jb.tmap)), "r"(0), "r"(r0), "r"(b)
+        : "memory");
+  }
+  // Full-width rows of 32/64/128 bytes come in through the tensor map with the matching
+  // 32/64/128-byte swizzle: 16-byte chunk q of row r sits at chunk q ^ (bits 7.. of the
+  // row's offset), so the 8 lanes of a quarter-warp reading chunk q of 8 consecutive rows
+  // hit 8 different bank groups (row-major stages are 2/4/8-way bank-conflicted).
+  static constexpr bool SWZ = (MM == 4 || MM == 8 || MM == 16);
+  static constexpr unsigned SWZ_MASK = (MM == 4) ? 1u : ((MM == 8) ? 3u : 7u);
+  template <bool FULLM>
+  __device__ __forceinline__ static double2 rd2(const unsigned char* stg, int r, int q, int m_) {
+    if constexpr (FULLM && SWZ) {
+      const unsigned off = (unsigned)r * (MM * 8) + (unsigned)q * 16u;
+      return *reinterpret_cast<const double2*>(stg + (off ^ (((off >> 7) & SWZ_MASK) << 4)));
+    } else {
+      return reinterpret_cast<const double2*>(stg + (size_t)r * m_ * 8)[q];
+    }
+  }
+  // One ring stage of SR rows starting at r0 (lane 0 issues).
+  template <bool FULLM>
+  __device__ __forceinline__ void issue_stage(unsigned char* dst, int r0, int n_, int m_,
+                                              unsigned long long* bar) const {
+    if (FULLM && SWZ) {
+      mbar_expect_tx(bar, (unsigned)SM::STAGE_BYTES);
+      tma_load_rows(dst, r0, bar);
+    } else {
+      const int nv = min(SM::SR, n_ - r0);
+      const unsigned bytes = (unsigned)(nv * m_ * 8);
+      mbar_expect_tx(bar, bytes);
+      tma_load_1d(dst, jb.scores + (size_t)r0 * m_, bytes, bar);
+    }
+  }
+
   // 256-bit load (sm_100: LDG.E.ENL2.256): a 4-model row in one instruction.  Volatile
   // on purpose: ptxas never reorders volatile accesses, so a group's loads (issued in
   // program order before the group's volatile smem stores) stay batched in flight —
@@ -698,15 +768,13 @@ struct Solver {
     constexpr int RL = SM::RL, SR = SM::SR, NSTG = L / RL;
     const bool tma = (m_ & 1) == 0;  // pass-uniform
     auto stage_row = [&](const int t) { return (t / NSTG) * TILE + wid_ * BLK + (t % NSTG) * SR; };
+    const unsigned gbase = SMX.stg_cnt[wid_];  // stage t is this warp's stage gbase + t
+    unsigned used = 0;
     auto issue = [&](const int t) {  // no-op past the last row
       const int r0 = stage_row(t);
-      if (lane_ == 0 && r0 < n_) {
-        const int nv = min(SR, n_ - r0);
-        const unsigned bytes = (unsigned)(nv * m_ * 8);
-        unsigned long long* bar = &SMX.stage_bar[wid_][t & 1];
-        mbar_expect_tx(bar, bytes);
-        tma_load_1d(SMX.ring[wid_][t & 1], sc + (size_t)r0 * m_, bytes, bar);
-      }
+      const unsigned g = gbase + (unsigned)t;
+      if (lane_ == 0 && r0 < n_)
+        issue_stage<FULLM>(SMX.ring[wid_][g & 1], r0, n_, m_, &SMX.stage_bar[wid_][g & 1]);
     };
     if (tma) issue(0);
     for (int k = 0; k < ntiles; ++k) {
@@ -768,17 +836,18 @@ struct Solver {
           const int t = k * NSTG + st;
           if (stage_row(t) >= n_) break;  // never issued: rows past the end stay b = 0
           issue(t + 1);  // the other slot was released by the __syncwarp below
-          mbar_wait(&SMX.stage_bar[wid_][t & 1], (t >> 1) & 1);
-          const unsigned char* stg = SMX.ring[wid_][t & 1];
+          const unsigned g = gbase + (unsigned)t;
+          mbar_wait(&SMX.stage_bar[wid_][g & 1], (g >> 1) & 1);
+          ++used;
+          const unsigned char* stg = SMX.ring[wid_][g & 1];
 #pragma unroll
           for (int i = 0; i < RL; ++i) {
             const int r = i * 32 + lane_;
             double v[MM];
-            const double2* rp = reinterpret_cast<const double2*>(stg + (size_t)r * m_ * 8);
 #pragma unroll
             for (int q = 0; q < MM / 2; ++q) {
               if (FULLM || 2 * q < m_) {
-                const double2 x = rp[q];
+                const double2 x = rd2<FULLM>(stg, r, q, m_);
                 v[2 * q] = x.x;
                 v[2 * q + 1] = x.y;
               } else {
@@ -946,6 +1015,7 @@ struct Solver {
         }
       }
     }
+    if (lane_ == 0) SMX.stg_cnt[wid_] = gbase + used;  // every issued stage was consumed
   }
 
   // g(alpha) = (sum_j best_j + sum_i alpha_i c_i) / N   (score_dual.cpp:47-48)
@@ -1064,42 +1134,32 @@ struct Solver {
     const int m_ = FULLM ? MM : jb.m;
     const int i = (I >= 0) ? I : i_rt;
     constexpr int SR = SM::SR, RL = SM::RL;
-    __syncthreads();  // every stage of the previous sweep / pass has been consumed
-    if (tid == 0) {
-      for (int w2 = 0; w2 < WP; ++w2)
-        for (int q = 0; q < 2; ++q) mbar_init(&SMX.stage_bar[w2][q], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     if (wid >= WP) return;
-    const double* __restrict__ sc = jb.scores;
+    const unsigned gbase = SMX.stg_cnt[wid];  // stage t is this warp's stage gbase + t
     auto row0 = [&](const int t) { return (t * WP + wid) * SR; };
     auto issue = [&](const int t) {
       const int r0 = row0(t);
-      if (lane == 0 && r0 < n) {
-        const int nv = min(SR, n - r0);
-        const unsigned bytes = (unsigned)(nv * m_ * 8);
-        unsigned long long* bar = &SMX.stage_bar[wid][t & 1];
-        mbar_expect_tx(bar, bytes);
-        tma_load_1d(SMX.ring[wid][t & 1], sc + (size_t)r0 * m_, bytes, bar);
-      }
+      const unsigned g = gbase + (unsigned)t;
+      if (lane == 0 && r0 < n)
+        issue_stage<FULLM>(SMX.ring[wid][g & 1], r0, n, m_, &SMX.stage_bar[wid][g & 1]);
     };
     issue(0);
+    int t = 0;
 #pragma unroll 1
-    for (int t = 0; row0(t) < n; ++t) {
+    for (; row0(t) < n; ++t) {
       issue(t + 1);  // the other slot was released by the __syncwarp below
-      mbar_wait(&SMX.stage_bar[wid][t & 1], (t >> 1) & 1);
-      const unsigned char* stg = SMX.ring[wid][t & 1];
+      const unsigned g = gbase + (unsigned)t;
+      mbar_wait(&SMX.stage_bar[wid][g & 1], (g >> 1) & 1);
+      const unsigned char* stg = SMX.ring[wid][g & 1];
       const int r0 = row0(t);
 #pragma unroll
       for (int ii = 0; ii < RL; ++ii) {
         const int r = ii * 32 + lane;
-        const double2* rp = reinterpret_cast<const double2*>(stg + (size_t)r * m_ * 8);
         double v[MM];
 #pragma unroll
         for (int q = 0; q < MM / 2; ++q) {
           if (FULLM || 2 * q < m_) {
-            const double2 x = rp[q];
+            const double2 x = rd2<FULLM>(stg, r, q, m_);
             v[2 * q] = x.x;
             v[2 * q + 1] = x.y;
           } else {
@@ -1116,10 +1176,12 @@ struct Solver {
             else rest = smax(rest, __dsub_rn(v[q], a[q]));
           }
         }
-        f(r0 + r < n, __dsub_rn(vi, rest));  // rows past the end: stale bytes, masked
+        f(r0 + r < n, __dsub_rn(vi, rest));  // rows past the end: zero / stale, masked
       }
       __syncwarp();  // every lane is done with this slot before it is refilled
     }
+    __syncwarp();
+    if (lane == 0) SMX.stg_cnt[wid] = gbase + (unsigned)t;
   }
   template <bool FULLM, int I, class F>
   __device__ __forceinline__ void polish_sweep_any(int i, const double (&a)[MM], F& f) {
@@ -1161,7 +1223,7 @@ struct Solver {
 
   // r-th largest (1-based) among the nc <= CAP keys in SMX.cand -> SMX.sel_prefix.
   __device__ void select_in_cand(int nc, int r) {
-    if (nc <= 128) {  // rank by comparison: one barrier
+    if (nc <= 384) {  // rank by comparison: one barrier
       for (int x = tid; x < nc; x += T) {
         const unsigned long long kx = SMX.cand[x];
         int gt = 0, ge = 0;
@@ -1195,6 +1257,7 @@ struct Solver {
   }
 
   static constexpr int NSH = 5;  // nested windows a_i +- d * 8^s (value space)
+  static constexpr int PTARGET = 96;  // polish: keys aimed for inside the inner window
   static_assert(2 * NSH <= 16, "red_i stride");
   struct CountWin {
     double lo[NSH], hi[NSH];
@@ -1428,14 +1491,15 @@ struct Solver {
         const double next = dkey_inv(SMX.sel_prefix);
         SMX.max_delta = smax(SMX.max_delta, fabs(__dsub_rn(next, SMX.polished[i])));
         SMX.polished[i] = next;
-        // adapt the window: aim for a hit with a few hundred candidates
+        // adapt the window to the measured key density around a_i: ~PTARGET keys inside
+        // +-d next time (a hit needs the k-th largest inside and <= CAP keys), widened to
+        // cover this move when that stays affordable (moves shrink as the polish converges)
         double d = SMX.pol_delta[i];
-        if (miss && nin > SM::CAP && gt_k_in) d *= 0.125;  // the window itself overflowed
-        else if (miss) d = fmin(fmax(d * 2.0, 1.5 * fabs(__dsub_rn(next, ai))), 4.0);
-        else if (nc > 512) d *= 0.25;
-        else if (nc > 128) d *= 0.5;
-        else if (nc < 24) d = fmin(d * 2.0, 4.0);
-        SMX.pol_delta[i] = fmax(d, 1e-300);
+        const double mv = fabs(__dsub_rn(next, ai));
+        const double dens = (double)nin / d;  // keys per unit of d (both sides)
+        d = (nin > 0) ? (double)PTARGET / dens : d * 8.0;
+        if (2.0 * mv > d && dens * 2.0 * mv <= (double)(SM::CAP / 2)) d = 2.0 * mv;
+        SMX.pol_delta[i] = fmin(fmax(d, 1e-300), 4.0);
         if (miss) SMX.prof[PR_PMISS]++;
         if (miss == 3) SMX.prof[PR_PRADIX]++;
         if (miss && gt_k_in) SMX.prof[PR_POVER]++;
@@ -1598,12 +1662,13 @@ struct Solver {
     unsigned long long kcut;  // key < kcut taken
     unsigned long long ktie;  // and key == ktie with j < jcut (when jcut > 0)
     unsigned jcut;
+    int cap;
     Solver* s;
     __device__ __forceinline__ void operator()(unsigned long long key, int j, int v) {
       const bool in = key < kcut || (jcut > 0 && key == ktie && (unsigned)j < jcut);
       if (in) {
         const int pos = atomicAdd(&s->smx().cand_n, 1);
-        if (pos < P1BUF) {
+        if (pos < cap) {
           s->smx().cand[2 * pos] = key;
           s->smx().cand[2 * pos + 1] = ((unsigned long long)(unsigned)j << 8) | (unsigned)v;
         }
@@ -1628,9 +1693,13 @@ struct Solver {
     return stop;
   }
 
-  __device__ void phase1_batch() {
-    // threshold: narrow the loss key one 8-bit digit per sweep while the smallest bin alone
-    // overflows the buffer; at full key depth narrow on j among equal losses
+  // The `cap` smallest candidates (key, j, v) of a candidate stream, sorted ascending by
+  // (key, j, v) into SMX.cand as (key, j << 8 | v) pairs; returns how many (<= cap).
+  // sw(f) calls f(key, j, v) for every candidate.  Threshold: narrow the key one 8-bit
+  // digit per sweep while the smallest bin alone overflows the buffer; at full key depth
+  // narrow on j among equal keys.  Then one gather sweep and a bitonic sort in smem.
+  template <class SW>
+  __device__ int select_smallest(SW& sw, const int cap) {
     unsigned long long pre = 0ull, kcut = ~0ull, ktie = 0ull;
     unsigned jcut = 0u, jpre = 0u;
     int shift = 56;
@@ -1640,10 +1709,10 @@ struct Solver {
       if (tid < 256) SMX.hist[tid] = 0u;
       __syncthreads();
       P1Hist h{pre, shift, jpre, this};
-      phase1_sweep(h);
+      sw(h);
       __syncthreads();
       if (tid == 0) {
-        const int stop = p1_pick(P1BUF, 0);
+        const int stop = p1_pick(cap, 0);
         const int cum = SMX.cand_over;
         int next = 0;  // 0: done, 1: descend
         if (shift >= 0) {
@@ -1701,10 +1770,10 @@ struct Solver {
     __syncthreads();
     if (tid == 0) SMX.cand_n = 0;
     __syncthreads();
-    P1Gather gth{kcut, ktie, jcut, this};
-    phase1_sweep(gth);
+    P1Gather gth{kcut, ktie, jcut, cap, this};
+    sw(gth);
     __syncthreads();
-    const int nb = min(SMX.cand_n, P1BUF);
+    const int nb = min(SMX.cand_n, cap);
     int np2 = 1;
     while (np2 < nb) np2 <<= 1;
     for (int q = nb + tid; q < np2; q += T) {
@@ -1732,6 +1801,18 @@ struct Solver {
       }
     }
     __syncthreads();
+    return nb;
+  }
+
+  struct P1Sweep {  // Phase-1 candidates of the current deltas
+    Solver* s;
+    template <class F>
+    __device__ __forceinline__ void operator()(F& f) { s->phase1_sweep(f); }
+  };
+
+  __device__ void phase1_batch() {
+    P1Sweep sw{this};
+    const int nb = select_smallest(sw, P1BUF);
     if (tid == 0) {
       for (int q = 0; q < nb; ++q) {
         bool any = false;
@@ -1822,6 +1903,141 @@ struct Solver {
     }
   }
 
+  // ---- repair Phase 2 lists (see repair) ------------------------------------------------
+  struct Ph2Hdr {
+    int head, len, complete;  // L: sorted best members at the last refresh, [head, len) live
+    int ehead, elen, need;    // E: sorted rows that joined u since; need: E overflowed
+  };
+  struct Ph2 {
+    double *Lg, *Eg;
+    int *Lj, *Ej;
+    Ph2Hdr* h;
+    int K, EC;
+  };
+  __device__ Ph2 ph2_ws() const {  // this CTA's slot of the Phase-2 workspace
+    unsigned char* b = jb.ws_ph2 + (size_t)blockIdx.x * (size_t)jb.ph2_stride;
+    const size_t P = (size_t)m * m;
+    Ph2 w;
+    w.K = jb.ph2_k;
+    w.EC = jb.ph2_ec;
+    w.Lg = reinterpret_cast<double*>(b);
+    w.Eg = w.Lg + P * w.K;
+    w.Lj = reinterpret_cast<int*>(w.Eg + P * w.EC);
+    w.Ej = w.Lj + P * w.K;
+    w.h = reinterpret_cast<Ph2Hdr*>(w.Ej + P * w.EC);
+    return w;
+  }
+  // Thread 0: gain / witness of every pair from the list heads into SMX.gain / witness;
+  // returns a pair whose max is not known (list dry before all members seen, or E
+  // overflowed), else -1.
+  __device__ int ph2_gains(Ph2& w) {
+    for (int u = 0; u < m; ++u)
+      for (int v = 0; v < m; ++v) {
+        if (u == v) continue;
+        const int p = u * m + v;
+        Ph2Hdr& h = w.h[p];
+        if (h.need) return p;
+        const double* Lg = w.Lg + (size_t)p * w.K;
+        const int* Lj = w.Lj + (size_t)p * w.K;
+        while (h.head < h.len && mo[Lj[h.head]] != u) ++h.head;
+        const bool haveL = h.head < h.len;
+        if (!haveL && !h.complete) return p;
+        double g = haveL ? Lg[h.head] : -CUDART_INF;
+        int jw = haveL ? Lj[h.head] : -1;
+        const double* Eg = w.Eg + (size_t)p * w.EC;
+        const int* Ej = w.Ej + (size_t)p * w.EC;
+        while (h.ehead < h.elen && mo[Ej[h.ehead]] != u) ++h.ehead;
+        if (h.ehead < h.elen) {
+          const double eg = Eg[h.ehead];
+          const int ej = Ej[h.ehead];
+          if (jw < 0 || eg > g || (eg == g && ej < jw)) {
+            g = eg;
+            jw = ej;
+          }
+        }
+        SMX.gain[p] = g;
+        SMX.witness[p] = jw;
+      }
+    return -1;
+  }
+  // Thread 0: move prompt j to model v (score_dual.cpp:86-93) and file it in the joined
+  // lists of every pair (v, x).
+  __device__ void ph2_move(Ph2& w, int j, int v) {
+    const int u = mo[j];
+    mo[j] = (uint8_t)v;
+    SMX.counts[u]--;
+    SMX.counts[v]++;
+    SMX.delta[u]--;
+    SMX.delta[v]++;
+    const double* row = jb.scores + (size_t)j * m;
+    const double sv = row[v];
+    for (int x = 0; x < m; ++x) {
+      if (x == v) continue;
+      Ph2Hdr& h = w.h[v * m + x];
+      if (h.need) continue;
+      double* Eg = w.Eg + (size_t)(v * m + x) * w.EC;
+      int* Ej = w.Ej + (size_t)(v * m + x) * w.EC;
+      if (h.elen == w.EC && h.ehead > 0) {  // drop the dead prefix
+        for (int q = h.ehead; q < h.elen; ++q) {
+          Eg[q - h.ehead] = Eg[q];
+          Ej[q - h.ehead] = Ej[q];
+        }
+        h.elen -= h.ehead;
+        h.ehead = 0;
+      }
+      if (h.elen == w.EC) {
+        h.need = 1;  // refreshed before its next use
+        continue;
+      }
+      const double g = __dsub_rn(row[x], sv);
+      int q = h.elen;
+      while (q > h.ehead && (Eg[q - 1] < g || (Eg[q - 1] == g && Ej[q - 1] > j))) {
+        Eg[q] = Eg[q - 1];
+        Ej[q] = Ej[q - 1];
+        --q;
+      }
+      Eg[q] = g;
+      Ej[q] = j;
+      h.elen++;
+    }
+  }
+  struct PairSweep {  // members j of model u as candidates (key(s_ju - s_jv), j, v)
+    Solver* s;
+    int u, v;
+    template <class F>
+    __device__ __forceinline__ void operator()(F& f) {
+      const int m_ = s->m;
+      for (int j = s->tid; j < s->n; j += T) {
+        if (s->mo[j] != u) continue;
+        const double* row = s->jb.scores + (size_t)j * m_;
+        f(dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))), j, v);
+      }
+    }
+  };
+  // CTA: rebuild pair (u, v)'s list as its best K members by (gain desc, j asc) — the K
+  // smallest (s_ju - s_jv, j) — exactly, and empty its joined list.
+  __device__ void ph2_refresh(Ph2& w, int u, int v) {
+    PairSweep sw{this, u, v};
+    const int nb = select_smallest(sw, w.K);
+    const int p = u * m + v;
+    for (int q = tid; q < nb; q += T) {
+      const int j = (int)(SMX.cand[2 * q + 1] >> 8);
+      const double* row = jb.scores + (size_t)j * m;
+      w.Lg[(size_t)p * w.K + q] = __dsub_rn(row[v], row[u]);
+      w.Lj[(size_t)p * w.K + q] = j;
+    }
+    if (tid == 0) {
+      Ph2Hdr& h = w.h[p];
+      h.head = 0;
+      h.len = nb;
+      h.complete = nb == SMX.counts[u];
+      h.ehead = h.elen = 0;
+      h.need = 0;
+      SMX.prof[PR_P2REFRESH]++;
+    }
+    __syncthreads();
+  }
+
   // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
     const long long t_rep = clock64();
@@ -1847,12 +2063,46 @@ struct Solver {
       }
       if (tid == 0) SMX.prof[PR_MOVES] += 1;
     }
-    // Phase 2: profitable 2- and 3-cycles (:120-180)
+    // Phase 2: profitable 2- and 3-cycles (:120-180).  The reference recomputes every
+    // gain[u][v] = max_{j in u} (s_jv - s_ju) (first j as witness) with a full sweep per
+    // applied cycle — thousands of sweeps on tie-heavy data.  Here one sweep seeds each
+    // (u, v) with its max; afterwards each pair keeps a list of its best members
+    // (ph2_refresh: the top K by (gain desc, j asc), exact) plus a sorted list of rows that
+    // joined u since, and a pass only looks at list heads.  Rows leave lazily (an entry is
+    // live iff mo[j] == u); a pair whose list ran dry before all members were seen is
+    // refreshed.  Same cycles, same witnesses, same order as the reference.
     if (m >= 2) {
+      Ph2 w = ph2_ws();
+      phase2_gains();
+      if (tid == 0) {
+        for (int u = 0; u < m; ++u)
+          for (int v = 0; v < m; ++v) {
+            if (u == v) continue;
+            const int p = u * m + v;
+            const int jw = SMX.witness[p];
+            Ph2Hdr& h = w.h[p];
+            h.head = 0;
+            h.len = jw >= 0 ? 1 : 0;
+            h.complete = jw < 0;  // u has no members
+            h.ehead = h.elen = 0;
+            h.need = 0;
+            if (jw >= 0) {
+              w.Lg[(size_t)p * w.K] = SMX.gain[p];
+              w.Lj[(size_t)p * w.K] = jw;
+            }
+          }
+      }
+      __syncthreads();
       for (int pass_i = 0; pass_i < 10000; ++pass_i) {
         if (tid == 0) SMX.prof[PR_P2PASSES]++;
-        phase2_gains();
-        __syncthreads();
+        for (;;) {  // every pair's max known exactly, refreshing lists that ran dry
+          if (tid == 0) SMX.flag = ph2_gains(w);
+          __syncthreads();
+          const int pr = SMX.flag;
+          __syncthreads();
+          if (pr < 0) break;
+          ph2_refresh(w, pr / m, pr % m);
+        }
         if (tid == 0) {
           double best = 1e-15;
           int cu = -1, cv = -1, cw = -1;
@@ -1869,38 +2119,30 @@ struct Solver {
           for (int u = 0; u < m; ++u)
             for (int v = 0; v < m; ++v) {
               if (v == u) continue;
-              for (int w = 0; w < m; ++w) {
-                if (w == u || w == v) continue;
-                double g = __dadd_rn(__dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + w]),
-                                     SMX.gain[w * m + u]);
+              for (int x = 0; x < m; ++x) {
+                if (x == u || x == v) continue;
+                double g = __dadd_rn(__dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + x]),
+                                     SMX.gain[x * m + u]);
                 if (g > best) {
                   best = g;
                   cu = u;
                   cv = v;
-                  cw = w;
+                  cw = x;
                 }
               }
             }
           SMX.flag = (cu < 0);
           if (cu >= 0) {
-            auto move = [&](int j, int v) {
-              int uu = mo[j];
-              mo[j] = (uint8_t)v;
-              SMX.counts[uu]--;
-              SMX.counts[v]++;
-              SMX.delta[uu]--;
-              SMX.delta[v]++;
-            };
             if (cw < 0) {
-              int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cu];
-              move(j1, cv);
-              move(j2, cu);
+              const int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cu];
+              ph2_move(w, j1, cv);
+              ph2_move(w, j2, cu);
             } else {
-              int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cw],
-                  j3 = SMX.witness[cw * m + cu];
-              move(j1, cv);
-              move(j2, cw);
-              move(j3, cu);
+              const int j1 = SMX.witness[cu * m + cv], j2 = SMX.witness[cv * m + cw],
+                        j3 = SMX.witness[cw * m + cu];
+              ph2_move(w, j1, cv);
+              ph2_move(w, j2, cw);
+              ph2_move(w, j3, cu);
             }
           }
         }
@@ -2308,8 +2550,9 @@ struct Solver {
 
 // ---------------------------------------------------------------------------------------
 template <int MM, int L, int T>
-__global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kernel(const Job jb) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1)
+    solver_kernel(const __grid_constant__ Job jb) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   using SM = Smem<MM, L, T>;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
   const int slot = blockIdx.x;
@@ -2317,7 +2560,17 @@ __global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1) solver_kern
   Solver<MM, L, T> s(jb, mo);
   const int tid = threadIdx.x;
   const int m = jb.m, n = jb.n;
-  if (tid == 0) sm.memo_valid = 0;
+  if (tid == 0) {
+    sm.memo_valid = 0;
+    for (int w2 = 0; w2 < SM::WP; ++w2) {  // stage barriers: once per launch
+      sm.stg_cnt[w2] = 0;
+      for (int q = 0; q < 2; ++q) {
+        const unsigned a = (unsigned)__cvta_generic_to_shared(&sm.stage_bar[w2][q]);
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(1) : "memory");
+      }
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
 
   if (jb.kind == JOB_SWEEP) {

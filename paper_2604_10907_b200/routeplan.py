@@ -656,6 +656,27 @@ def engine(device: int = 0) -> Engine:
         return _ENGINES[device]
 
 
+def sweep_multi(engines: Sequence["Engine"], profile_index, setup_ids, taus,
+                opt: OptimizeContext, params) -> np.ndarray:
+    """rw_sweep_multi: the sweep sharded over several engines (one host thread per GPU);
+    records in instance order, bit-identical to a one-engine sweep_slo."""
+    pi = np.ascontiguousarray(profile_index, np.int32).reshape(-1)
+    m = engines[0].m
+    S = len(pi) // max(m, 1)
+    ids = np.ascontiguousarray(setup_ids if setup_ids is not None else np.arange(S), np.int64)
+    t = np.ascontiguousarray(taus, np.float64)
+    plist = params if isinstance(params, (list, tuple)) else [params] * len(t)
+    bps = (_abi.rw_beta_params * len(t))(*[q.c() for q in plist])
+    hs = (C.c_void_p * len(engines))(*[e.h.value for e in engines])
+    recs = np.zeros(max(S * len(t), 1), dtype=_abi.RECORD_DTYPE)
+    oc = opt.c()
+    rc = _abi.lib().rw_sweep_multi(hs, len(engines), S, lptr(ids), iptr(pi), len(t), dptr(t),
+                                   C.byref(oc), bps, C.c_void_p(recs.ctypes.data))
+    if rc:
+        _raise(rc, _abi.lib().rw_last_error(engines[0].h).decode())
+    return recs[: S * len(t)]
+
+
 def reduce_records(records: np.ndarray) -> int:
     """setup_search.cpp:246-253 over records from any shards -> index or -1."""
     r = np.ascontiguousarray(records, dtype=_abi.RECORD_DTYPE)

@@ -68,3 +68,35 @@ def test_reference_acceptance_numbers_match_cpu_build():
         if k in (4, 5, 8):  # criteria on functions the shim does not replace
             continue
         assert _numbers_without_timing(gpu[k][1]) == _numbers_without_timing(cpu[k][1]), k
+
+
+PAR_B200 = os.path.join(ROOT, "integration", "_build", "parallel_check_b200")
+PAR_REF = os.path.join(ROOT, "integration", "_build", "parallel_check_ref")
+
+
+def _dumps(exe, env=None):
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, **(env or {})))
+    assert out.returncode == 0, out.stdout + out.stderr
+    runs = []
+    for block in out.stdout.split("end\n"):
+        lines = [ln for ln in block.splitlines() if ln.strip()]
+        if lines:
+            runs.append((lines[0], lines[1:]))
+    return runs
+
+
+@pytest.mark.gpu
+def test_multi_gpu_select_setup_bit_identical_to_reference():
+    """SearchParams::parallelism -> GPU shards (rw_sweep_multi: one host thread per GPU,
+    interleaved setups, records combined in setup order).  With RW_SHIM_SHARED_GPU=1 the
+    2- and 3-shard runs put their contexts on the one visible GPU; every run must equal the
+    unmodified reference select_setup bit for bit (test_setup_search.cpp:264-292)."""
+    ref = _dumps(PAR_REF)
+    gpu = _dumps(PAR_B200, {"RW_SHIM_SHARED_GPU": "1"})
+    assert len(ref) == 1 and len(gpu) == 3
+    assert len(ref[0][1]) == 65  # 64 sweep rows + the plan
+    for head, body in gpu:
+        assert body == ref[0][1], head

@@ -258,3 +258,40 @@ def test_eval_pass_full_size_vs_oracle(eng, oracle, name):
         g_ref, counts_ref, mo_ref = oracle.eval_dual(s, c, alpha)
         assert bits(g) == bits(g_ref)
         assert np.array_equal(counts, counts_ref) and np.array_equal(mo, mo_ref)
+
+
+def _solve_vs_oracle(eng, oracle, s, c, sub_iters=20):
+    from oracle import Params
+    eng.load_scores(s)
+    got = eng.solve_dual(c, rw.SubgradientParams(1.0, sub_iters, 1e-12, 4))
+    ref = oracle.solve_dual(s, c, Params(sub_max_iters=sub_iters))
+    assert np.array_equal(bits(got.alpha_star.alpha), bits(ref["alpha"]))
+    assert bits(got.score) == bits(ref["score"]), (got.score, ref["score"])
+    assert bits(got.dual_bound) == bits(ref["dual_bound"])
+    assert np.array_equal(np.asarray(got.assignment), ref["assignment"])
+    assert got.eval_passes == ref["eval_passes"]
+    return got, ref
+
+
+@pytest.mark.parametrize("n", [30_000, 100_000])
+def test_solve_dual_c5_ties_repair_vs_oracle(eng, oracle, n):
+    """C5's adversarial ties at integral targets: repair Phase 2 runs thousands of cycles
+    (score_dual.cpp:120-180) — the incremental pair lists must pick the same witnesses in
+    the same order as the reference's full re-sweeps."""
+    cfg = wl.config("C5", n=n)
+    s = wl.scores_for(cfg)
+    c = np.full(cfg.m, n / cfg.m)
+    _solve_vs_oracle(eng, oracle, s, c)
+
+
+def test_polish_tie_group_larger_than_candidate_buffer(eng, oracle):
+    """more than 4096 rows share the k-th largest b of a polish coordinate (the
+    overfull-shell narrowing ends on one key value): the answer is that value."""
+    n = 20_000
+    rng = np.random.default_rng(3)
+    s = np.empty((n, 2))
+    s[:, 0] = 0.5
+    s[:, 1] = 0.25
+    s[18_000:, 1] = rng.uniform(0.0, 1.0, n - 18_000)
+    for c in ([10_000.0, 10_000.0], [4_000.0, 16_000.0], [9_999.5, 10_000.5]):
+        _solve_vs_oracle(eng, oracle, s, np.array(c))
