@@ -161,7 +161,7 @@ int rw_last_kernel_ms(const rw_ctx* ctx, double* ms);
 /* Diagnostics: counters summed over CTAs and over the launches since the last read
  * (RW_PROF_SLOTS entries; see rw_solver.cuh `Prof` for the slot meanings: pass phase
  * cycles, block classification counts, walker cycles, polish cycles and misses). */
-#define RW_PROF_SLOTS 24
+#define RW_PROF_SLOTS 32
 int rw_set_profiling(rw_ctx* ctx, int enable);
 int rw_get_profile(rw_ctx* ctx, int64_t* out);
 /* Diagnostics: `passes` eval passes at fixed prices on one CTA (per-pass cost probe). */

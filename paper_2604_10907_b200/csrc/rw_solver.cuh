@@ -98,6 +98,11 @@ enum Prof {
   PR_PSHELL = 20,    // polish: in a middle shell (second sweep gathers it)
   PR_PMOVE = 21,     // polish: sum over coordinates of round(log2(|move| / d)) + 64
   PR_P2REFRESH = 22, // repair Phase 2: pair lists rebuilt
+  PR_P1CYC = 23,     // repair Phase 1 (cycles)
+  PR_P2CYC = 24,     // repair Phase 2 without list refreshes (cycles)
+  PR_REFCYC = 25,    // repair Phase 2 list refreshes (cycles)
+  PR_P2SEED = 26,    // repair Phase 2 seeding sweep (cycles)
+  PR_PHIST = 27,     // polish: overfull shells resolved by the value-bin histogram sweep
 };
 struct Piece {
   long long q;
@@ -1257,7 +1262,7 @@ struct Solver {
   }
 
   static constexpr int NSH = 5;  // nested windows a_i +- d * 8^s (value space)
-  static constexpr int PTARGET = 96;  // polish: keys aimed for inside the inner window
+  static constexpr int PTARGET = 256;  // polish: keys aimed for inside the inner window
   static_assert(2 * NSH <= 16, "red_i stride");
   struct CountWin {
     double lo[NSH], hi[NSH];
@@ -1318,6 +1323,61 @@ struct Solver {
       s->hist_add(ok && key >= lo && key <= hi, (unsigned)((key >> shift) & 0xffull));
     }
   };
+  static constexpr int NB4 = 4096;  // value bins of the overfull-shell histogram
+  __device__ __forceinline__ static int vbin(double b, double vlo, double inv) {
+    const double x = floor(__dmul_rn(__dsub_rn(b, vlo), inv));
+    return x < 0.0 ? 0 : (x >= (double)(NB4 - 1) ? NB4 - 1 : (int)x);
+  }
+  struct HistBins {  // histogram of the keys in [lo, hi] over value bins of [vlo, vhi]
+    unsigned long long lo, hi;
+    double vlo, inv;
+    unsigned* h;
+    __device__ __forceinline__ void operator()(bool ok, double bv) {
+      const unsigned long long key = dkey(bv);
+      if (ok && key >= lo && key <= hi) atomicAdd(&h[vbin(bv, vlo, inv)], 1u);
+    }
+  };
+  struct GatherBin {  // keys in [lo, hi] whose value bin is `bin`
+    unsigned long long lo, hi;
+    double vlo, inv;
+    int bin;
+    Solver* s;
+    __device__ __forceinline__ void operator()(bool ok, double bv) {
+      const unsigned long long key = dkey(bv);
+      s->gather(ok && key >= lo && key <= hi && vbin(bv, vlo, inv) == bin, key);
+    }
+  };
+  // Warp 0: the value bin (of NB4, counted from the top) holding the k-th largest ->
+  // SMX.sel_lo (bin), SMX.sel_k (rank inside it), SMX.cand_over (its count).
+  __device__ void pick_bin4k(int k) {
+    if (wid != 0) return;
+    const unsigned* h = reinterpret_cast<const unsigned*>(SMX.cand);
+    constexpr int PER = NB4 / 32;
+    const int top = NB4 - 1 - PER * lane;  // lane l covers bins [top - PER + 1, top]
+    int local = 0;
+    for (int q = 0; q < PER; ++q) local += (int)h[top - q];
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(FULL, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int excl = incl - local;
+    if (excl < k && k <= incl) {
+      int above = excl;
+      for (int q = 0; q < PER; ++q) {
+        const int c = (int)h[top - q];
+        if (above + c >= k) {
+          SMX.sel_lo = (unsigned long long)(top - q);
+          SMX.sel_k = k - above;
+          SMX.cand_over = c;
+          break;
+        }
+        above += c;
+      }
+    }
+  }
+
   // Warp 0: the digit bin holding the k-th largest counted key -> SMX.sel_lo (bin),
   // SMX.sel_k (rank inside the bin), SMX.cand_over (the bin's count).
   __device__ void pick_bin(int k) {
@@ -1405,6 +1465,15 @@ struct Solver {
         miss = 1;
         unsigned long long lo = 0ull, hi = ~0ull;
         int r = k, cnt = 0, above = 0;
+        // the shell's value range (for the histogram sweep); b is bounded by the score range:
+        // b = s_ji - max_{q != i}(s_jq - a_q) in [-1 + min a_q, 1 + max a_q] for s in [0, 1]
+        double amin = CUDART_INF, amax = -CUDART_INF;
+        for (int q = 0; q < m; ++q)
+          if (q != i) {
+            amin = fmin(amin, a[q]);
+            amax = fmax(amax, a[q]);
+          }
+        double vlo = 0.0, vhi = 0.0;
         for (int z = 0; z < 2 * NSH + 1; ++z) {
           int c;
           // b > x  <=>  dkey(b) > dkey(x): value-space shells as key ranges
@@ -1413,15 +1482,21 @@ struct Solver {
             c = (q == NSH - 1 ? cw.gt[q] : cw.gt[q] - cw.gt[q + 1]);
             lo = dkey(cw.hi[q]) + 1;
             hi = (q == NSH - 1) ? ~0ull : dkey(cw.hi[q + 1]);
+            vlo = cw.hi[q];
+            vhi = (q == NSH - 1) ? fmax(1.0 + amax, cw.hi[q]) : cw.hi[q + 1];
           } else if (z == NSH) {
             c = nin;
             lo = dkey(cw.lo[0]);
             hi = dkey(cw.hi[0]);
+            vlo = cw.lo[0];
+            vhi = cw.hi[0];
           } else {  // below shells: [lo[q+1], lo[q]) from the inside out
             const int q = z - NSH - 1;
             c = (q == NSH - 1 ? cw.lt[q] : cw.lt[q] - cw.lt[q + 1]);
             lo = (q == NSH - 1) ? 0ull : dkey(cw.lo[q + 1]);
             hi = dkey(cw.lo[q]) - 1;
+            vlo = (q == NSH - 1) ? fmin(-1.0 + amin, cw.lo[q]) : cw.lo[q + 1];
+            vhi = cw.lo[q];
           }
           if (above + c >= k) {
             r = k - above;
@@ -1441,12 +1516,40 @@ struct Solver {
           nc = SMX.cand_n;
           select_in_cand(nc, r);
         } else {
-          // the shell is too full for smem: narrow it one 8-bit key digit per sweep,
-          // starting at the first digit where its bounds differ, until the digit bucket
-          // holding the r-th key fits — then gather that bucket and select in smem
           miss = 3;
+          // the shell is too full for smem: one sweep histograms it into NB4 equal value
+          // bins (bin(b) is monotone in b, so bins are value-ordered groups), a second
+          // gathers the bin holding the r-th largest — three sweeps in all, whatever the move
+          bool done = false;
+          const double inv = (vhi > vlo) ? (double)NB4 / (vhi - vlo) : 0.0;
+          {
+            unsigned* h4 = reinterpret_cast<unsigned*>(SMX.cand);
+            __syncthreads();
+            for (int q = tid; q < NB4; q += T) h4[q] = 0u;
+            if (tid == 0) SMX.cand_over = 0x7fffffff;  // "not found" -> digit narrowing
+            __syncthreads();
+            HistBins hb{lo, hi, vlo, inv, h4};
+            polish_sweep<FULLM>(i, a, hb);
+            __syncthreads();
+            pick_bin4k(r);  // -> SMX.sel_lo (bin), sel_k (rank in it), cand_over (its count)
+            __syncthreads();
+            const int bsel = (int)SMX.sel_lo, rb = SMX.sel_k, cb = SMX.cand_over;
+            __syncthreads();
+            if (cb <= SM::CAP) {
+              if (tid == 0) SMX.cand_n = 0;
+              __syncthreads();
+              GatherBin gb{lo, hi, vlo, inv, bsel, this};
+              polish_sweep<FULLM>(i, a, gb);
+              __syncthreads();
+              nc = SMX.cand_n;
+              select_in_cand(nc, rb);
+              done = true;
+            }
+            if (tid == 0) SMX.prof[PR_PHIST]++;
+          }
+          // one bin still too full (massive exact ties): narrow by 8-bit key digits
           unsigned long long plo = lo, phi = hi;
-          int rk = r, cnt_b = cnt;
+          int rk = r, cnt_b = done ? 0 : cnt;
           int shift = (lo == hi) ? 0 : ((63 - __clzll((long long)(lo ^ hi))) / 8) * 8;
           while (cnt_b > SM::CAP && plo != phi) {
             __syncthreads();
@@ -1469,7 +1572,8 @@ struct Solver {
             if (shift < 0) break;
           }
           __syncthreads();
-          if (plo == phi) {
+          if (done) {
+          } else if (plo == phi) {
             // every key left is the same value (e.g. > CAP exact ties of the k-th largest
             // on quantised scores): that value is the answer, no gather needed
             if (tid == 0) SMX.sel_prefix = plo;
@@ -1914,12 +2018,27 @@ struct Solver {
     Ph2Hdr* h;
     int K, EC;
   };
-  __device__ Ph2 ph2_ws() const {  // this CTA's slot of the Phase-2 workspace
-    unsigned char* b = jb.ws_ph2 + (size_t)blockIdx.x * (size_t)jb.ph2_stride;
+  // Where the lists live.  The TMA ring is idle during repair Phase 2 (its sweeps use plain
+  // loads), so for small M the lists sit in it — every bookkeeping access of the serial
+  // cycle loop is then a shared-memory access; larger M use this CTA's global slot.
+  static constexpr int PH2_EC_SMEM = 16;
+  __device__ Ph2 ph2_ws() const {
     const size_t P = (size_t)m * m;
+    const size_t ring = sizeof(SMX.ring);
+    const long long ksm =
+        ((long long)ring - (long long)P * (PH2_EC_SMEM * 12 + (long long)sizeof(Ph2Hdr))) /
+        ((long long)P * 12);
     Ph2 w;
-    w.K = jb.ph2_k;
-    w.EC = jb.ph2_ec;
+    unsigned char* b;
+    if (ksm >= 32) {
+      b = &SMX.ring[0][0][0];
+      w.K = (int)min(ksm, (long long)P1BUF);
+      w.EC = PH2_EC_SMEM;
+    } else {
+      b = jb.ws_ph2 + (size_t)blockIdx.x * (size_t)jb.ph2_stride;
+      w.K = jb.ph2_k;
+      w.EC = jb.ph2_ec;
+    }
     w.Lg = reinterpret_cast<double*>(b);
     w.Eg = w.Lg + P * w.K;
     w.Lj = reinterpret_cast<int*>(w.Eg + P * w.EC);
@@ -1927,39 +2046,106 @@ struct Solver {
     w.h = reinterpret_cast<Ph2Hdr*>(w.Ej + P * w.EC);
     return w;
   }
-  // Thread 0: gain / witness of every pair from the list heads into SMX.gain / witness;
-  // returns a pair whose max is not known (list dry before all members seen, or E
-  // overflowed), else -1.
-  __device__ int ph2_gains(Ph2& w) {
-    for (int u = 0; u < m; ++u)
-      for (int v = 0; v < m; ++v) {
-        if (u == v) continue;
-        const int p = u * m + v;
-        Ph2Hdr& h = w.h[p];
-        if (h.need) return p;
-        const double* Lg = w.Lg + (size_t)p * w.K;
-        const int* Lj = w.Lj + (size_t)p * w.K;
-        while (h.head < h.len && mo[Lj[h.head]] != u) ++h.head;
-        const bool haveL = h.head < h.len;
-        if (!haveL && !h.complete) return p;
-        double g = haveL ? Lg[h.head] : -CUDART_INF;
-        int jw = haveL ? Lj[h.head] : -1;
-        const double* Eg = w.Eg + (size_t)p * w.EC;
-        const int* Ej = w.Ej + (size_t)p * w.EC;
-        while (h.ehead < h.elen && mo[Ej[h.ehead]] != u) ++h.ehead;
-        if (h.ehead < h.elen) {
-          const double eg = Eg[h.ehead];
-          const int ej = Ej[h.ehead];
-          if (jw < 0 || eg > g || (eg == g && ej < jw)) {
-            g = eg;
-            jw = ej;
-          }
-        }
-        SMX.gain[p] = g;
-        SMX.witness[p] = jw;
+  // Warp 0 (one lane per pair): gain / witness of every pair from the list heads into
+  // SMX.gain / witness; sets SMX.flag to a pair whose max is not known (list dry before all
+  // members were seen, or E overflowed), else -1.
+  __device__ void ph2_gains(Ph2& w) {
+    if (wid != 0) return;
+    int need = 0x7fffffff;
+    for (int p = lane; p < m * m; p += 32) {
+      const int u = p / m, v = p % m;
+      if (u == v) continue;
+      Ph2Hdr& h = w.h[p];
+      if (h.need) {
+        need = min(need, p);
+        continue;
       }
-    return -1;
+      const double* Lg = w.Lg + (size_t)p * w.K;
+      const int* Lj = w.Lj + (size_t)p * w.K;
+      int hd = h.head;
+      while (hd < h.len && mo[Lj[hd]] != u) ++hd;
+      h.head = hd;
+      const bool haveL = hd < h.len;
+      if (!haveL && !h.complete) {
+        need = min(need, p);
+        continue;
+      }
+      double g = haveL ? Lg[hd] : -CUDART_INF;
+      int jw = haveL ? Lj[hd] : -1;
+      const double* Eg = w.Eg + (size_t)p * w.EC;
+      const int* Ej = w.Ej + (size_t)p * w.EC;
+      int eh = h.ehead;
+      while (eh < h.elen && mo[Ej[eh]] != u) ++eh;
+      h.ehead = eh;
+      if (eh < h.elen) {
+        const double eg = Eg[eh];
+        const int ej = Ej[eh];
+        if (jw < 0 || eg > g || (eg == g && ej < jw)) {
+          g = eg;
+          jw = ej;
+        }
+      }
+      SMX.gain[p] = g;
+      SMX.witness[p] = jw;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) need = min(need, __shfl_xor_sync(FULL, need, off));
+    if (lane == 0) SMX.flag = (need == 0x7fffffff) ? -1 : need;
   }
+  // Thread 0: fold pair p's joined list E into its best-member list L (both sorted by
+  // (gain desc, j asc)), keeping at most K entries.  Invariant of an incomplete L: every
+  // member of u in neither list ranks after L's tail (its last entry at the refresh, dead or
+  // alive).  So from E only the entries ranking before that tail may join L (the others
+  // become such unlisted members); entries cut off at K rank after the new tail.
+  __device__ void ph2_merge(Ph2& w, int p) {
+    Ph2Hdr& h = w.h[p];
+    double* Lg = w.Lg + (size_t)p * w.K;
+    int* Lj = w.Lj + (size_t)p * w.K;
+    const double* Eg = w.Eg + (size_t)p * w.EC;
+    const int* Ej = w.Ej + (size_t)p * w.EC;
+    const bool have_tail = h.len > 0;
+    const double tg = have_tail ? Lg[h.len - 1] : 0.0;
+    const int tj = have_tail ? Lj[h.len - 1] : 0;
+    auto before_tail = [&](double g, int j) {  // ranks strictly before the refresh tail
+      return h.complete || (have_tail && (g > tg || (g == tg && j < tj)));
+    };
+    int nl = 0;  // L's live window to the front
+    for (int q = h.head; q < h.len; ++q) {
+      Lg[nl] = Lg[q];
+      Lj[nl] = Lj[q];
+      ++nl;
+    }
+    int eb = h.elen;  // E's usable entries are a prefix of its sorted window
+    while (eb > h.ehead && !before_tail(Eg[eb - 1], Ej[eb - 1])) --eb;
+    const int ne = eb - h.ehead;
+    int total = nl + ne;
+    bool complete = h.complete && eb == h.elen;
+    if (total > w.K) {
+      total = w.K;
+      complete = false;
+    }
+    int a = nl - 1, b = eb - 1;  // merge from the back
+    for (int o = nl + ne - 1; o >= 0; --o) {
+      bool takeE;
+      if (a < 0) takeE = true;
+      else if (b < h.ehead) takeE = false;
+      else takeE = (Eg[b] < Lg[a]) || (Eg[b] == Lg[a] && Ej[b] > Lj[a]);  // E[b] ranks later
+      const double g = takeE ? Eg[b] : Lg[a];
+      const int jj = takeE ? Ej[b] : Lj[a];
+      if (takeE) --b;
+      else --a;
+      if (o < total) {
+        Lg[o] = g;
+        Lj[o] = jj;
+      }
+    }
+    h.head = 0;
+    h.len = total;
+    h.complete = complete;
+    h.ehead = h.elen = 0;
+    if (!complete && total == 0) h.need = 1;  // nothing usable left: refresh
+  }
+
   // Thread 0: move prompt j to model v (score_dual.cpp:86-93) and file it in the joined
   // lists of every pair (v, x).
   __device__ void ph2_move(Ph2& w, int j, int v) {
@@ -1985,6 +2171,7 @@ struct Solver {
         h.elen -= h.ehead;
         h.ehead = 0;
       }
+      if (h.elen == w.EC) ph2_merge(w, v * m + x);  // E full: fold it into L
       if (h.elen == w.EC) {
         h.need = 1;  // refreshed before its next use
         continue;
@@ -2014,12 +2201,81 @@ struct Solver {
       }
     }
   };
-  // CTA: rebuild pair (u, v)'s list as its best K members by (gain desc, j asc) — the K
-  // smallest (s_ju - s_jv, j) — exactly, and empty its joined list.
+  // CTA: rebuild pair (u, v)'s list — an exact prefix of its members in (gain desc, j asc)
+  // order, i.e. ascending (key(s_ju - s_jv), j) — and empty its joined list.  Tie-heavy
+  // data (C5) has large groups of equal gains: the members tied at the best gain, taken in
+  // j order (first K), are such a prefix and cost two sweeps (the best key, then an ordered
+  // gather that stops at K).  When that group is small the generic selection
+  // (select_smallest: digit narrowing, then gather and sort) fills the list to K instead.
   __device__ void ph2_refresh(Ph2& w, int u, int v) {
-    PairSweep sw{this, u, v};
-    const int nb = select_smallest(sw, w.K);
     const int p = u * m + v;
+    unsigned long long kmin = ~0ull;
+    for (int j = tid; j < n; j += T) {
+      if (mo[j] != u) continue;
+      const double* row = jb.scores + (size_t)j * m;
+      const unsigned long long key = dkey(__dsub_rn(__ldg(row + u), __ldg(row + v)));
+      kmin = key < kmin ? key : kmin;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(FULL, kmin, off);
+      kmin = o < kmin ? o : kmin;
+    }
+    __syncthreads();
+    if (lane == 0) SMX.red_i[wid] = 0;
+    unsigned long long* kred = reinterpret_cast<unsigned long long*>(SMX.red_d);
+    if (lane == 0) kred[wid] = kmin;
+    __syncthreads();
+    for (int w2 = 0; w2 < W; ++w2) kmin = kred[w2] < kmin ? kred[w2] : kmin;
+    // members with key == kmin in increasing j, the first K (chunks of R rows per thread)
+    constexpr int R = 4;
+    int got = 0;
+    for (int base = 0; base < n && got < w.K; base += T * R) {
+      int hit[R];
+      int c = 0;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        const int j = base + tid * R + q;
+        hit[q] = 0;
+        if (j < n && mo[j] == u) {
+          const double* row = jb.scores + (size_t)j * m;
+          hit[q] = dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))) == kmin;
+        }
+        c += hit[q];
+      }
+      int incl = c;  // block exclusive prefix of c in thread (= row) order
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t2 = __shfl_up_sync(FULL, incl, off);
+        if (lane >= off) incl += t2;
+      }
+      __syncthreads();
+      if (lane == 31) SMX.red_i[wid] = incl;
+      __syncthreads();
+      int before = got;
+      for (int w2 = 0; w2 < wid; ++w2) before += SMX.red_i[w2];
+      int total = got;
+      for (int w2 = 0; w2 < W; ++w2) total += SMX.red_i[w2];
+      int pos = before + incl - c;
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (hit[q]) {
+          if (pos < w.K) {
+            SMX.cand[2 * pos] = kmin;
+            SMX.cand[2 * pos + 1] = ((unsigned long long)(unsigned)(base + tid * R + q) << 8) |
+                                    (unsigned)v;
+          }
+          ++pos;
+        }
+      }
+      got = total;
+    }
+    __syncthreads();
+    int nb = min(got, w.K);
+    if (nb < min(64, w.K) && nb < SMX.counts[u]) {  // small best-gain group: fill to K
+      PairSweep sw{this, u, v};
+      nb = select_smallest(sw, w.K);
+    }
     for (int q = tid; q < nb; q += T) {
       const int j = (int)(SMX.cand[2 * q + 1] >> 8);
       const double* row = jb.scores + (size_t)j * m;
@@ -2052,6 +2308,7 @@ struct Solver {
     // threshold under which at most P1BUF candidates lie, gather and sort them, and apply
     // them in order while they stay eligible — candidates above the threshold cannot
     // precede any of them.  A couple of sweeps per batch instead of one per move.
+    const long long tp1 = clock64();
     for (;;) {
       int surplus = 0;
       for (int i = 0; i < m; ++i) surplus += SMX.delta[i] > 0 ? SMX.delta[i] : 0;
@@ -2071,9 +2328,12 @@ struct Solver {
     // joined u since, and a pass only looks at list heads.  Rows leave lazily (an entry is
     // live iff mo[j] == u); a pair whose list ran dry before all members were seen is
     // refreshed.  Same cycles, same witnesses, same order as the reference.
+    if (tid == 0) SMX.prof[PR_P1CYC] += clock64() - tp1;
     if (m >= 2) {
+      const long long tp2 = clock64();
       Ph2 w = ph2_ws();
       phase2_gains();
+      if (tid == 0) SMX.prof[PR_P2SEED] += clock64() - tp2;
       if (tid == 0) {
         for (int u = 0; u < m; ++u)
           for (int v = 0; v < m; ++v) {
@@ -2096,12 +2356,14 @@ struct Solver {
       for (int pass_i = 0; pass_i < 10000; ++pass_i) {
         if (tid == 0) SMX.prof[PR_P2PASSES]++;
         for (;;) {  // every pair's max known exactly, refreshing lists that ran dry
-          if (tid == 0) SMX.flag = ph2_gains(w);
+          ph2_gains(w);
           __syncthreads();
           const int pr = SMX.flag;
           __syncthreads();
           if (pr < 0) break;
+          const long long tr = clock64();
           ph2_refresh(w, pr / m, pr % m);
+          if (tid == 0) SMX.prof[PR_REFCYC] += clock64() - tr;
         }
         if (tid == 0) {
           double best = 1e-15;
@@ -2150,6 +2412,10 @@ struct Solver {
         if (SMX.flag) break;
         __syncthreads();
       }
+      // the lists may have lived in the TMA ring: order these generic-proxy writes before
+      // the next pass's bulk copies into it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (tid == 0) SMX.prof[PR_P2CYC] += clock64() - tp2;
     }
     __syncthreads();
     // exact sequential mean of the repaired assignment (:182-184)

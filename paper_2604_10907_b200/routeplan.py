@@ -475,7 +475,7 @@ class Engine:
         self._chk(self.L.rw_set_profiling(self.h, 1 if enable else 0))
 
     def profile(self) -> np.ndarray:
-        out = np.zeros(24, np.int64)
+        out = np.zeros(32, np.int64)
         self._chk(self.L.rw_get_profile(self.h, lptr(out)))
         return out
 
