@@ -122,6 +122,21 @@ def ref_params(p):
                   beta_max=p.beta_max, epsilon=p.epsilon)
 
 
+def loaded_native_libs():
+    """Native libraries of this repo mapped into this process (the reference arm must map
+    only oracle/ ones)."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                path = ln.split()[-1] if ln.strip() else ""
+                if path.startswith(ROOT) and path.endswith(".so"):
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
 def cpu_model():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -297,7 +312,8 @@ def reference_arm(args):
                                        f"parallelism={threads}, {passes} eval passes; "
                                        f"warm-up steps: 1 setup at N={small.n}"},
             "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "native_libs_mapped": loaded_native_libs()}
     print(json.dumps(line), flush=True)
 
 

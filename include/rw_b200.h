@@ -171,7 +171,10 @@ int rw_bench_passes(rw_ctx* ctx, const double* targets, const double* alpha, int
 /* ---- inputs ------------------------------------------------------------------------ */
 /* Copy the N x M score matrix from host memory into the ctx's HBM buffer
  * (replaces ScoreMatrix ownership, workload.hpp:12-23; values validated like
- * ScoreMatrix::validate, workload.cpp:12-30). */
+ * ScoreMatrix::validate, workload.cpp:12-30).  The copy is enqueued on the ctx stream and
+ * the call returns without waiting for it: from page-locked (pinned) memory it overlaps
+ * whatever runs before it on the stream; the caller keeps host_scores unchanged until the
+ * next synchronising call (rw_sweep_fetch, any solver entry point). */
 int rw_load_scores(rw_ctx* ctx, int32_t n, int32_t m, const double* host_scores);
 /* Borrow an already-resident device matrix (caller keeps it alive). */
 int rw_bind_scores_device(rw_ctx* ctx, int32_t n, int32_t m, const double* device_scores);
@@ -265,6 +268,20 @@ int rw_sweep_multi(rw_ctx* const* ctxs, int32_t n_ctx, int64_t n_setups,
  * latency, then smallest setup_id.  Records may come from any number of shards in any
  * order.  Returns the record index or -1. */
 int64_t rw_reduce_records(int64_t n, const rw_setup_record* records);
+
+/* ---- f2: binary score files ------------------------------------------ */
+/* The reference reads scores from CSV (load_scores, workload.cpp:32-62).  A .f64 score
+ * file ("RWSCORE1" | int64 n | int64 m | m x (int32 len, name) | n*m float64 row-major)
+ * is one read; pair it with rw_load_scores from a pinned buffer for an asynchronous H2D.
+ * Entries are validated like ScoreMatrix::validate (workload.cpp:23-29); a missing or
+ * malformed file is RW_ERR_CONFIG (the reference's ConfigError for inputs).  Messages:
+ * rw_host_last_error(). */
+int rw_write_scores_f64(const char* path, int64_t n, int32_t m, const char* const* models,
+                        const double* scores);
+/* out == NULL: header only (n, m, names '\0'-separated into names[names_cap]). */
+int rw_read_scores_f64(const char* path, int64_t* n, int32_t* m, double* out, int64_t out_cap,
+                       char* names, int64_t names_cap);
+const char* rw_host_last_error(void);
 
 /* ---- host-side input producers ------------------------------------------------------ */
 /* workload.cpp:78-112 synth_scores: Beta(a_i, b_i) columns via mt19937_64 + libstdc++

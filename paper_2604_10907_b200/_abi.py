@@ -146,6 +146,11 @@ def lib():
                                      C.POINTER(rw_beta_params), C.c_void_p]
         L.rw_set_records_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.rw_reduce_records.argtypes = [C.c_int64, C.c_void_p]
+        L.rw_write_scores_f64.argtypes = [C.c_char_p, C.c_int64, C.c_int32,
+                                          C.POINTER(C.c_char_p), _dp]
+        L.rw_read_scores_f64.argtypes = [C.c_char_p, _lp, _ip, _dp, C.c_int64, C.c_char_p,
+                                         C.c_int64]
+        L.rw_host_last_error.restype = C.c_char_p
         L.rw_synth_scores.argtypes = [C.c_int32, C.c_int32, _dp, _dp, C.c_uint64, _dp]
         L.rw_enumerate_retain.argtypes = [C.c_int32, _ip, _ip, _ip, _ip, _dp, C.c_int32, _ip,
                                           _ip, _dp, C.c_int32, C.c_double, C.c_int64, _lp, _ip,

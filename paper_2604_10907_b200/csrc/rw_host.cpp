@@ -4,8 +4,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "rw_b200.h"
@@ -16,6 +19,104 @@ constexpr double kEps = 1e-9;  // setup_search.cpp:16
 }  // namespace
 
 extern "C" {
+
+// ---- f2: binary score files ---------------------------------------------
+// The reference ingests scores as CSV (load_scores, workload.cpp:32-62: one strtod per
+// entry — 160M of them at 10M x 16).  A .f64 score file is one read:
+//   "RWSCORE1" | int64 n | int64 m | m x (int32 len, name bytes) | n*m float64, row-major
+// (little-endian; scores[j * m + i] as workload.hpp:15).  Entries are validated like
+// ScoreMatrix::validate (workload.cpp:23-29): finite and inside [0, 1].
+static const char kMagic[8] = {'R', 'W', 'S', 'C', 'O', 'R', 'E', '1'};
+
+const char* rw_host_last_error(void) { return g_host_err.c_str(); }
+
+int rw_write_scores_f64(const char* path, int64_t n, int32_t m, const char* const* models,
+                        const double* scores) {
+  if (!path || n < 1 || m < 1 || !scores) return RW_ERR_VALIDATION;
+  FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_host_err = std::string("cannot write ") + path;
+    return RW_ERR_CONFIG;
+  }
+  const int64_t hdr[2] = {n, (int64_t)m};
+  bool ok = std::fwrite(kMagic, 1, 8, f) == 8 && std::fwrite(hdr, 8, 2, f) == 2;
+  for (int i = 0; ok && i < m; ++i) {
+    const char* name = models ? models[i] : "";
+    const int32_t len = (int32_t)std::strlen(name);
+    ok = std::fwrite(&len, 4, 1, f) == 1 && std::fwrite(name, 1, len, f) == (size_t)len;
+  }
+  ok = ok && std::fwrite(scores, sizeof(double), (size_t)n * m, f) == (size_t)n * m;
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) g_host_err = std::string("short write to ") + path;
+  return ok ? RW_OK : RW_ERR_CONFIG;
+}
+
+// Header only when out == NULL (n, m and the names, '\0'-separated, into names[cap]).
+int rw_read_scores_f64(const char* path, int64_t* n_out, int32_t* m_out, double* out,
+                       int64_t out_cap, char* names, int64_t names_cap) {
+  FILE* f = path ? std::fopen(path, "rb") : nullptr;
+  if (!f) {
+    g_host_err = std::string(path ? path : "(null)") + ": cannot open score file";
+    return RW_ERR_CONFIG;  // a missing input file is a ConfigError in the reference
+  }
+  char magic[8];
+  int64_t hdr[2];
+  int rc = RW_OK;
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kMagic, 8) != 0 ||
+      std::fread(hdr, 8, 2, f) != 2 || hdr[0] < 1 || hdr[1] < 1 || hdr[1] > (1 << 20)) {
+    g_host_err = std::string(path) + ": not a RWSCORE1 score file";
+    std::fclose(f);
+    return RW_ERR_CONFIG;
+  }
+  const int64_t n = hdr[0], m = hdr[1];
+  std::vector<std::string> model(m);
+  int64_t used = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    int32_t len = 0;
+    if (std::fread(&len, 4, 1, f) != 1 || len < 0 || len > 4096) rc = RW_ERR_CONFIG;
+    if (rc) break;
+    model[i].resize(len);
+    if (len && std::fread(&model[i][0], 1, len, f) != (size_t)len) rc = RW_ERR_CONFIG;
+    if (names && used + len + 1 <= names_cap) {
+      std::memcpy(names + used, model[i].data(), len);
+      names[used + len] = '\0';
+    }
+    used += len + 1;
+  }
+  if (rc) {
+    g_host_err = std::string(path) + ": truncated header";
+    std::fclose(f);
+    return rc;
+  }
+  if (n_out) *n_out = n;
+  if (m_out) *m_out = (int32_t)m;
+  if (!out) {
+    std::fclose(f);
+    return RW_OK;
+  }
+  if (out_cap < n * m) {
+    std::fclose(f);
+    g_host_err = "rw_read_scores_f64: output buffer too small";
+    return RW_ERR_VALIDATION;
+  }
+  if (std::fread(out, sizeof(double), (size_t)(n * m), f) != (size_t)(n * m)) {
+    std::fclose(f);
+    g_host_err = std::string(path) + ": truncated score data";
+    return RW_ERR_CONFIG;
+  }
+  std::fclose(f);
+  for (int64_t k = 0; k < n * m; ++k) {  // ScoreMatrix::validate (workload.cpp:23-29)
+    const double v = out[k];
+    if (!std::isfinite(v) || v < 0.0 || v > 1.0) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%.17g", v);
+      g_host_err = "score matrix: entry for prompt 'p" + std::to_string(k / m + 1) +
+                   "', model '" + model[k % m] + "' is " + buf + ", outside [0, 1]";
+      return RW_ERR_VALIDATION;
+    }
+  }
+  return RW_OK;
+}
 
 // workload.cpp:78-112: column i ~ Beta(a_i, b_i) = X/(X+Y), X~Gamma(a_i), Y~Gamma(b_i); one
 // mt19937_64 for the whole matrix, columns drawn in model order, rows in prompt order.
@@ -66,7 +167,17 @@ int rw_enumerate_retain(int32_t m, const int32_t* name_rank, const int32_t* tp_o
   int64_t total = 1;
   for (const auto& c : choice) total *= static_cast<int64_t>(c.size());
   *n_enum = total;
+  // Every candidate's verdict is independent: the enumeration range is split over host
+  // threads (f1), each running the odometer from its chunk's first id.
+  auto run_range = [&](int64_t lo, int64_t hi) -> int {
   std::vector<size_t> idx(m, 0);
+  {
+    int64_t rem = lo;  // mixed-radix digits of lo, model 0 most significant
+    for (int pos = m - 1; pos >= 0; --pos) {
+      idx[pos] = (size_t)(rem % (int64_t)choice[pos].size());
+      rem /= (int64_t)choice[pos].size();
+    }
+  }
   struct Shard {
     int model;
     double frac;
@@ -75,7 +186,7 @@ int rw_enumerate_retain(int32_t m, const int32_t* name_rank, const int32_t* tp_o
   std::vector<size_t> order;
   std::vector<double> remaining;
   std::vector<uint64_t> occupied;  // bit per model (m <= 64)
-  for (int64_t id = 0; id < total && id < cap; ++id) {
+  for (int64_t id = lo; id < hi; ++id) {
     // demand window (:146-148)
     double demand = 0.0;
     for (int i = 0; i < m; ++i) demand += choice[i][idx[i]].first * choice[i][idx[i]].second;
@@ -131,6 +242,19 @@ int rw_enumerate_retain(int32_t m, const int32_t* name_rank, const int32_t* tp_o
       idx[pos] = 0;
     }
   }
+  return RW_OK;
+  };
+  const int64_t count = std::min(total, cap);
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  const int nt = (int)std::min<int64_t>(hw, std::max<int64_t>(1, count / 4096));
+  if (nt <= 1) return run_range(0, count);
+  std::vector<int> rcs(nt, RW_OK);
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] { rcs[t] = run_range(count * t / nt, count * (t + 1) / nt); });
+  for (auto& th : pool) th.join();
+  for (int rc : rcs)
+    if (rc != RW_OK) return rc;  // the first failing chunk in enumeration order
   return RW_OK;
 }
 

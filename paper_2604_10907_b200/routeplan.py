@@ -836,6 +836,32 @@ def synth_scores(n_prompts: int, models: Sequence[str], shapes: Sequence[Tuple[f
     return ScoreMatrix([f"p{j + 1}" for j in range(n_prompts)], list(models), out)
 
 
+def write_scores_f64(matrix: ScoreMatrix, path: str) -> None:
+    """f2: the score matrix as a RWSCORE1 binary file (rw_write_scores_f64)."""
+    a = np.ascontiguousarray(matrix.scores, np.float64)
+    n, m = a.shape
+    names = (C.c_char_p * m)(*[s.encode() for s in matrix.models])
+    rc = _abi.lib().rw_write_scores_f64(path.encode(), n, m, names, dptr(a))
+    if rc:
+        _raise(rc, _abi.lib().rw_host_last_error().decode())
+
+
+def read_scores_f64(path: str) -> ScoreMatrix:
+    """f2: a RWSCORE1 binary score file -> ScoreMatrix (validated like the CSV loader)."""
+    L = _abi.lib()
+    n, m = C.c_int64(), C.c_int32()
+    names = C.create_string_buffer(1 << 16)
+    rc = L.rw_read_scores_f64(path.encode(), C.byref(n), C.byref(m), None, 0, names, len(names))
+    if rc:
+        _raise(rc, L.rw_host_last_error().decode())
+    out = np.empty((n.value, m.value), np.float64)
+    rc = L.rw_read_scores_f64(path.encode(), None, None, dptr(out), out.size, None, 0)
+    if rc:
+        _raise(rc, L.rw_host_last_error().decode())
+    models = names.raw.split(b"\0")[: m.value]
+    return ScoreMatrix([f"p{j + 1}" for j in range(n.value)], [x.decode() for x in models], out)
+
+
 def enumerate_retain(space: SetupSpace, gpu_count: int, rho_floor: float, mem: MemoryTable):
     """enumerate_setups + retain (setup_search.cpp:99-152) on the host C++ path.
 

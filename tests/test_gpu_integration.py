@@ -100,3 +100,29 @@ def test_multi_gpu_select_setup_bit_identical_to_reference():
     assert len(ref[0][1]) == 65  # 64 sweep rows + the plan
     for head, body in gpu:
         assert body == ref[0][1], head
+
+
+RUN_B200 = os.path.join(ROOT, "integration", "_build", "runner_check_b200")
+RUN_REF = os.path.join(ROOT, "integration", "_build", "runner_check_ref")
+
+
+@pytest.mark.gpu
+def test_runner_outputs_byte_identical_to_cpu_build(tmp_path):
+    """f3: the reference's own runner (run_plan / run_sweep, runner.cpp:151-173)
+    rendering plan.txt and sweep.csv (render_plan / render_sweep_csv, format_double;
+    runner.cpp:69-149, csv.cpp:78-84) on top of the GPU path must write the same bytes as
+    the unmodified CPU build — the drop-in's output path, not just its numbers."""
+    for exe in (RUN_B200, RUN_REF):
+        if not os.path.exists(exe):
+            pytest.skip(f"{exe} not built")
+    outs = {}
+    for name, exe in (("gpu", RUN_B200), ("cpu", RUN_REF)):
+        d = tmp_path / name
+        d.mkdir()
+        r = subprocess.run([exe, str(d)], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout + r.stderr
+        outs[name] = {f: (d / f).read_bytes() for f in ("plan.txt", "sweep.csv")}
+    assert b"status = FEASIBLE" in outs["cpu"]["plan.txt"]
+    assert outs["gpu"]["plan.txt"] == outs["cpu"]["plan.txt"]
+    assert outs["gpu"]["sweep.csv"] == outs["cpu"]["sweep.csv"]
+    assert outs["cpu"]["sweep.csv"].count(b"\n") == 65  # header + 64 retained setups

@@ -295,3 +295,26 @@ def test_polish_tie_group_larger_than_candidate_buffer(eng, oracle):
     s[18_000:, 1] = rng.uniform(0.0, 1.0, n - 18_000)
     for c in ([10_000.0, 10_000.0], [4_000.0, 16_000.0], [9_999.5, 10_000.5]):
         _solve_vs_oracle(eng, oracle, s, np.array(c))
+
+
+def test_binary_file_and_pinned_async_load_give_identical_sweeps(eng, tmp_path):
+    """f2: scores through a .f64 file and a page-locked host buffer (rw_load_scores enqueues
+    the H2D and returns) give the same records as the in-memory path."""
+    import torch
+    from paper_2604_10907_b200 import routeplan as rp
+    cfg = wl.config("C2", n=20000)
+    inp = wl.build_inputs(cfg, limit=8)
+    s = wl.scores_for(cfg)
+    path = str(tmp_path / "c2.f64")
+    rp.write_scores_f64(rp.ScoreMatrix([f"p{j + 1}" for j in range(cfg.n)], cfg.models, s), path)
+    t = rp.read_scores_f64(path).scores
+    pinned = torch.from_numpy(t).pin_memory().numpy()
+    tau = cfg.taus[3]
+    bp = wl.with_span_epsilon(wl.truncated_params(), tau, 4.0)
+    opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=tau, kappa=cfg.kappa)
+    out = []
+    for src in (s, pinned):
+        eng.load_scores(src)
+        eng.load_profiles(inp.koff, inp.kx, inp.ky)
+        out.append(eng.sweep(inp.profile_index, inp.retained, opt, bp))
+    assert out[0].tobytes() == out[1].tobytes()
