@@ -264,6 +264,20 @@ int rw_sweep_multi(rw_ctx* const* ctxs, int32_t n_ctx, int64_t n_setups,
                    const double* tau_ms, const rw_opt_context* opt,
                    const rw_beta_params* params, rw_setup_record* out_records);
 
+/* f4: the same sweep with a speculative beta bisection.  optimize_beta
+ * (routing_opt.cpp:138-173) is sequential; each round here evaluates the next `depth`
+ * levels of every instance's bisection tree in one launch (depth 2: the midpoint and both
+ * midpoints the next step can take) and the host follows the realised path with the
+ * reference's bracket arithmetic.  Records are bit-identical to rw_sweep_slo's (same
+ * eval_passes = the reference trajectory's); exec_passes also counts the discarded
+ * branches.  For sweeps too small to fill the GPU (C1: 64 setups) it cuts the sequential
+ * depth of the default schedule's 10-11 bisection steps to 6 rounds.  depth 1..4;
+ * out_records holds n_setups * n_slo records in instance order. */
+int rw_sweep_spec(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
+                  const int32_t* profile_index, int32_t n_slo, const double* tau_ms,
+                  const rw_opt_context* opt, const rw_beta_params* params, int32_t depth,
+                  rw_setup_record* out_records, int64_t* n_out);
+
 /* Order-deterministic winner (setup_search.cpp:246-253): feasible, max score, then min
  * latency, then smallest setup_id.  Records may come from any number of shards in any
  * order.  Returns the record index or -1. */

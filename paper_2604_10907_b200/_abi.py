@@ -141,6 +141,9 @@ def lib():
                                          C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
                                          C.c_int32, C.c_int32]
         L.rw_sweep_fetch.argtypes = [C.c_void_p, C.c_void_p, _lp]
+        L.rw_sweep_spec.argtypes = [C.c_void_p, C.c_int64, _lp, _ip, C.c_int32, _dp,
+                                    C.POINTER(rw_opt_context), C.POINTER(rw_beta_params),
+                                    C.c_int32, C.c_void_p, _lp]
         L.rw_sweep_multi.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_int64, _lp, _ip,
                                      C.c_int32, _dp, C.POINTER(rw_opt_context),
                                      C.POINTER(rw_beta_params), C.c_void_p]

@@ -52,6 +52,11 @@ struct rw_ctx {
   rw_setup_record* d_records_user = nullptr;  // caller-owned device buffer (optional)
   int64_t records_user_cap = 0;
   int64_t pending_records = -1;
+  // speculative bisection (rw_sweep_spec)
+  void* d_items = nullptr;
+  size_t items_cap = 0;
+  void* d_frac = nullptr;
+  size_t frac_cap = 0;
   // timing
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   bool timed = false;
@@ -298,6 +303,8 @@ void rw_destroy(rw_ctx* ctx) {
   cudaFree(ctx->d_prof_idx);
   cudaFree(ctx->d_setup_ids);
   cudaFree(ctx->d_records);
+  cudaFree(ctx->d_items);
+  cudaFree(ctx->d_frac);
   cudaFree(ctx->d_prof);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -844,6 +851,212 @@ int rw_sweep_slo(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const 
                               shard_rank, shard_count);
   if (rc) return rc;
   return rw_sweep_fetch(ctx, out, n_out);
+}
+
+// ---- f4: speculative beta bisection --------------------------------------------------
+// optimize_beta (routing_opt.cpp:138-173) is a strictly sequential bisection: each step's
+// midpoint depends on the previous step's feasibility.  A round here evaluates, for every
+// instance, the next `depth` levels of the bisection tree at once (the midpoint and, for
+// depth 2, both midpoints the next step can take) in ONE launch of optimize_fractions items;
+// the host then walks each instance down the realised path, replaying the reference's
+// bracket arithmetic and trace bookkeeping exactly (setup_search.cpp:187-211).  Same
+// records, half the sequential depth at depth 2 — for sweeps too small to fill the GPU.
+namespace {
+struct SpecInst {
+  double lo, hi, eps, tau;
+  bool feasible = false, active = true;
+  int n_trace = 0, status = 0;
+  double tr_best_lat = 0.0, tr_best_score = 0.0, beta_star = 0.0;
+  rw::FracRecord best{};
+  bool degenerate = false;  // no bisection step: one optimize_fractions at beta_hi
+  rw::FracRecord degen{};
+  int64_t ev = 0, pol = 0, rep = 0, exec = 0;
+};
+}  // namespace
+
+int rw_sweep_spec(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids, const int32_t* pidx,
+                  int32_t n_slo, const double* taus, const rw_opt_context* opt,
+                  const rw_beta_params* params, int32_t depth, rw_setup_record* out,
+                  int64_t* n_out) {
+  int rc;
+  if ((rc = need_inputs(ctx, true))) return rc;
+  if (!opt || !params || !taus || !out)
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep_spec: null argument");
+  if (n_setups < 0 || n_slo < 1)
+    return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep: bad setup / SLO count");
+  if (depth < 1 || depth > 4) return set_err(ctx, RW_ERR_VALIDATION, "rw_sweep_spec: depth must be 1..4");
+  if (!(opt->lambda_rps > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "arrival rate must be positive");
+  if (!(opt->kappa > 0.0)) return set_err(ctx, RW_ERR_VALIDATION, "kappa must be positive");
+  const int64_t inst = n_setups * (int64_t)n_slo;
+  if (n_out) *n_out = inst;
+  if (inst == 0) return RW_OK;
+  for (int32_t t = 0; t < n_slo; ++t) {
+    rw_opt_context o = *opt;
+    o.tau_ms = taus[t];
+    if ((rc = check_beta_params(ctx, &o, params + t))) return rc;
+  }
+  if ((rc = validate_profile_index(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
+  CK(cudaSetDevice(ctx->device));
+  if ((rc = upload_pidx(ctx, pidx, (size_t)n_setups * ctx->m))) return rc;
+  {  // taus + per-SLO params, as rw_sweep_slo_async lays them out
+    void* p = ctx->d_setup_ids;
+    size_t cap = ctx->setup_ids_cap;
+    if ((rc = ensure(ctx, &p, &cap,
+                     sizeof(int64_t) * n_setups + (sizeof(double) + sizeof(rw_beta_params)) * n_slo +
+                         64)))
+      return rc;
+    ctx->d_setup_ids = static_cast<int64_t*>(p);
+    ctx->setup_ids_cap = cap;
+    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups, taus, sizeof(double) * n_slo,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups + n_slo, params,
+                       sizeof(rw_beta_params) * n_slo, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // routing_opt.cpp:142-151 bracket per instance (instance k = slo * n_setups + setup)
+  std::vector<SpecInst> st(inst);
+  for (int64_t k = 0; k < inst; ++k) {
+    const rw_beta_params& bp = params[k / n_setups];
+    SpecInst& s = st[k];
+    s.tau = taus[k / n_setups];
+    s.lo = bp.beta_min;
+    s.hi = bp.beta_max < 0.0 ? 10.0 / s.tau : bp.beta_max;
+    s.eps = bp.epsilon < 0.0 ? (s.hi - s.lo) / 1024.0 : bp.epsilon;
+    s.active = s.hi - s.lo > s.eps;
+    s.degenerate = !s.active;  // setup_search.cpp:203-208
+  }
+  std::vector<rw::FracItem> items;
+  std::vector<rw::FracRecord> res;
+  std::vector<std::vector<int64_t>> node_item(inst);  // per instance: item of tree node
+  bool first = true;
+  for (;;) {
+    items.clear();
+    for (int64_t k = 0; k < inst; ++k) {
+      SpecInst& s = st[k];
+      node_item[k].assign((size_t)1 << depth, -1);
+      if (first && s.degenerate) {  // the top penalty, once
+        node_item[k][0] = (int64_t)items.size();
+        items.push_back({(int32_t)(k % n_setups), (int32_t)(k / n_setups), s.hi});
+        continue;
+      }
+      if (!s.active) continue;
+      // breadth-first tree of brackets: node 1 = (lo, hi); children 2n (ok: hi = mid) and
+      // 2n + 1 (not ok: lo = mid); a node exists while its bracket is wider than eps
+      std::vector<double> nlo((size_t)1 << depth), nhi((size_t)1 << depth);
+      nlo[1] = s.lo;
+      nhi[1] = s.hi;
+      for (size_t nd = 1; nd < ((size_t)1 << depth); ++nd) {
+        if (nd > 1 && node_item[k][nd / 2] < 0) continue;  // parent absent
+        if (!(nhi[nd] - nlo[nd] > s.eps)) continue;
+        const double mid = 0.5 * (nlo[nd] + nhi[nd]);
+        node_item[k][nd] = (int64_t)items.size();
+        items.push_back({(int32_t)(k % n_setups), (int32_t)(k / n_setups), mid});
+        if (2 * nd + 1 < ((size_t)1 << depth)) {
+          nlo[2 * nd] = nlo[nd];
+          nhi[2 * nd] = mid;
+          nlo[2 * nd + 1] = mid;
+          nhi[2 * nd + 1] = nhi[nd];
+        }
+      }
+    }
+    if (items.empty()) break;
+    // one launch: every item is an independent optimize_fractions (persistent CTAs)
+    const size_t ni = items.size();
+    if ((rc = ensure(ctx, &ctx->d_items, &ctx->items_cap, sizeof(rw::FracItem) * ni))) return rc;
+    if ((rc = ensure(ctx, &ctx->d_frac, &ctx->frac_cap, sizeof(rw::FracRecord) * ni))) return rc;
+    CK(cudaMemcpyAsync(ctx->d_items, items.data(), sizeof(rw::FracItem) * ni,
+                       cudaMemcpyHostToDevice, ctx->stream));
+    const int grid = (int)std::min<int64_t>((int64_t)ni, rw::sweep_max_resident(ctx->m, ctx->device));
+    if ((rc = ensure_ws(ctx, grid))) return rc;
+    rw::Job j = base_job(ctx, rw::JOB_FRAC_BATCH);
+    j.prof_idx = ctx->d_prof_idx;
+    j.n_items = (int64_t)ni;
+    j.taus = reinterpret_cast<const double*>(ctx->d_setup_ids + n_setups);
+    j.bps = reinterpret_cast<const rw_beta_params*>(ctx->d_setup_ids + n_setups + n_slo);
+    j.opt = *opt;
+    j.bp = *params;
+    j.frac_items = static_cast<const rw::FracItem*>(ctx->d_items);
+    j.frac_out = static_cast<rw::FracRecord*>(ctx->d_frac);
+    if ((rc = run(ctx, j, grid))) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+    res.resize(ni);
+    CK(cudaMemcpy(res.data(), ctx->d_frac, sizeof(rw::FracRecord) * ni, cudaMemcpyDeviceToHost));
+    // walk each instance down its realised path (routing_opt.cpp:154-171)
+    for (int64_t k = 0; k < inst; ++k) {
+      SpecInst& s = st[k];
+      for (int64_t it : node_item[k])
+        if (it >= 0) s.exec += res[it].exec_passes;
+      if (first && s.degenerate) {
+        const rw::FracRecord& r = res[node_item[k][0]];
+        s.degen = r;
+        s.ev += r.eval_passes;
+        s.pol += r.polish_passes;
+        s.rep += r.repair_calls;
+        if (r.status && !s.status) s.status = r.status;
+        continue;
+      }
+      if (!s.active) continue;
+      size_t nd = 1;
+      while (nd < ((size_t)1 << depth) && node_item[k][nd] >= 0 && s.hi - s.lo > s.eps) {
+        const rw::FracRecord& r = res[node_item[k][nd]];
+        const double mid = 0.5 * (s.lo + s.hi);
+        s.ev += r.eval_passes;
+        s.pol += r.polish_passes;
+        s.rep += r.repair_calls;
+        if (r.status) {
+          if (!s.status) s.status = r.status;
+          s.active = false;
+          break;
+        }
+        bool in_range = r.out_of_range == 0u;
+        bool ok = r.latency_ms <= s.tau && in_range;
+        if (s.n_trace == 0 || r.latency_ms < s.tr_best_lat) {  // setup_search.cpp:200-202
+          s.tr_best_lat = r.latency_ms;
+          s.tr_best_score = r.score;
+        }
+        s.n_trace++;
+        if (ok) {
+          s.feasible = true;
+          s.beta_star = mid;
+          s.best = r;
+          s.hi = mid;
+          nd = 2 * nd;
+        } else {
+          s.lo = mid;
+          nd = 2 * nd + 1;
+        }
+      }
+      if (!(s.hi - s.lo > s.eps)) s.active = false;
+    }
+    first = false;
+  }
+  // records, as evaluate_setup writes them (setup_search.cpp:187-211)
+  for (int64_t k = 0; k < inst; ++k) {
+    const SpecInst& s = st[k];
+    rw_setup_record& r = out[k];
+    std::memset(&r, 0, sizeof r);
+    r.setup_id = setup_ids ? setup_ids[k % n_setups] : k % n_setups;
+    r.status = s.status;
+    r.feasible = (!s.status && s.feasible) ? 1 : 0;
+    const bool f = s.feasible;
+    r.score = f ? s.best.score : (s.n_trace > 0 ? s.tr_best_score : s.degen.score);
+    r.latency_ms = f ? s.best.latency_ms : (s.n_trace > 0 ? s.tr_best_lat : s.degen.latency_ms);
+    if (s.status) r.score = r.latency_ms = 0.0;
+    r.beta = f ? s.beta_star : 0.0;
+    r.tau_ms = s.tau;
+    for (int i = 0; i < RW_MAX_MODELS; ++i) r.w[i] = (f && i < ctx->m) ? s.best.w[i] : 0.0;
+    r.out_of_range = f ? s.best.out_of_range : 0u;
+    r.bisect_steps = s.n_trace;
+    r.eval_passes = s.ev;
+    r.polish_passes = s.pol;
+    r.repair_calls = s.rep;
+    r.exec_passes = s.exec;
+  }
+  for (int64_t k = 0; k < inst; ++k)
+    if (st[k].status)
+      return set_err(ctx, st[k].status,
+                     "setup " + std::to_string(out[k].setup_id) + ": solver status " +
+                         std::to_string(st[k].status));
+  return RW_OK;
 }
 
 int rw_sweep_multi(rw_ctx* const* ctxs, int32_t n_ctx, int64_t n_setups,

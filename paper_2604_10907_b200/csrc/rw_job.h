@@ -17,6 +17,22 @@ enum JobKind : int32_t {
   JOB_SIMPLEX = 5,  // project_simplex on one vector
   JOB_LATENCY = 6,  // system_latency_eval + grad for one setup
   JOB_BENCH_PASS = 7,  // diagnostics: trace_cap eval passes at fixed prices
+  JOB_FRAC_BATCH = 8,  // optimize_fractions over (setup, SLO, beta) items (speculative bisection)
+};
+
+// One optimize_fractions evaluation of a speculative beta bisection (rw_sweep_spec).
+struct FracItem {
+  int32_t setup;  // index into the sweep's setups
+  int32_t slo;    // index into taus / bps
+  double beta;
+};
+struct FracRecord {  // routing_opt.hpp:36-44 RelaxedSolveResult + counters
+  double w[RW_MAX_MODELS];
+  double score, latency_ms, objective;
+  int32_t iterations, converged;
+  uint32_t out_of_range;
+  int32_t status;
+  int64_t eval_passes, polish_passes, repair_calls, exec_passes;
 };
 
 struct Job {
@@ -66,6 +82,9 @@ struct Job {
   int32_t ph2_k, ph2_ec;
   unsigned long long* queue;
   long long* prof_out;  // optional diagnostics counters [RW_PROF_SLOTS]
+  // JOB_FRAC_BATCH
+  const FracItem* frac_items;  // [n_items]
+  FracRecord* frac_out;        // [n_items]
 };
 
 // Repair Phase-2 list geometry for m models: K best members per pair (<= the 2048-pair

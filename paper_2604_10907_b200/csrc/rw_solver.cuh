@@ -794,7 +794,7 @@ struct Solver {
       const double scale =
           pred_ok ? __longlong_as_double((long long)(52 - e_pred + 1023) << 52) : 1.0;
       long long Q = 0;
-      bool tie = false;
+      bool tie = false, neg = false;
       double sb = 0.0, sa = 0.0;
       const long long t0 = prof ? clock64() : 0;
       // -- loads + priced argmax + speculative quanta -----------------------------------
@@ -824,7 +824,7 @@ struct Solver {
         scr[g * 32 + lane_] = bj;
         Q += quanta(bj, scale, tie);
         sb += bj;
-        sa += fabs(bj);
+        neg |= bj < 0.0;
         const bool cnt = valid && want_counts;
         if (NPK == 1) {
           pk[0] += cnt ? (1ull << (arg * 16)) : 0ull;
@@ -930,7 +930,7 @@ struct Solver {
             st_shared_volatile(&scr[(g0 + gg) * 32 + lane_], bj);
             Q += quanta(bj, scale, tie);
             sb += bj;
-            sa += fabs(bj);
+            neg |= bj < 0.0;
             const bool cnt = valid && want_counts;
             if (NPK == 1) {
               pk[0] += cnt ? (1ull << (arg * 16)) : 0ull;
@@ -944,8 +944,18 @@ struct Solver {
         }
       }
       // -- block totals -> approximate prefix before this block ------------------------
+      // sum |b| for the margins: equal to sum b when no b is negative (same operands, same
+      // order) — the common case once the prices are gauged; otherwise from the smem copy
+      // (any order: the margin covers every summation order)
       sb = warp_sum_d(sb);
-      sa = warp_sum_d(sa);
+      if (__any_sync(FULL, neg)) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < L; ++q) t += fabs(scr[q * 32 + lane_]);
+        sa = warp_sum_d(t);
+      } else {
+        sa = sb;
+      }
       if (lane_ == 0) {
         SMX.tot_b[s][wid_] = sb;
         SMX.tot_a[s][wid_] = sa;
@@ -1261,7 +1271,7 @@ struct Solver {
     __syncthreads();
   }
 
-  static constexpr int NSH = 5;  // nested windows a_i +- d * 8^s (value space)
+  static constexpr int NSH = 3;  // nested windows a_i +- d * 8^s (value space)
   static constexpr int PTARGET = 256;  // polish: keys aimed for inside the inner window
   static_assert(2 * NSH <= 16, "red_i stride");
   struct CountWin {
@@ -2751,6 +2761,32 @@ struct Solver {
     }
   }
 
+  // ---- one speculative-bisection item: optimize_fractions at a given beta -------------
+  __device__ void evaluate_frac_item(const FracItem& it, FracRecord* out) {
+    rw_opt_context opt = jb.opt;
+    if (jb.taus) opt.tau_ms = jb.taus[it.slo];
+    const rw_beta_params bp = jb.bps ? jb.bps[it.slo] : jb.bp;
+    pidx = jb.prof_idx + (size_t)it.setup * m;
+    reset_counters();
+    optimize_fractions(it.beta, opt, bp.pga);
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 0; i < RW_MAX_MODELS; ++i) out->w[i] = i < m ? SMX.fr_w[i] : 0.0;
+      out->score = SMX.fr_score;
+      out->latency_ms = SMX.fr_lat;
+      out->objective = SMX.fr_obj;
+      out->iterations = SMX.fr_iters;
+      out->converged = SMX.fr_conv;
+      out->out_of_range = SMX.fr_oor;
+      out->status = SMX.status;
+      out->eval_passes = SMX.eval_passes;
+      out->polish_passes = SMX.polish_passes;
+      out->repair_calls = SMX.repair_calls;
+      out->exec_passes = SMX.exec_passes;
+    }
+    __syncthreads();
+  }
+
   __device__ void reset_counters() {
     if (tid == 0) {
       SMX.status = 0;
@@ -2839,6 +2875,18 @@ __global__ void __launch_bounds__(T, (MM <= 16 && T <= 256) ? 2 : 1)
   }
   __syncthreads();
 
+  if (jb.kind == JOB_FRAC_BATCH) {  // persistent over the items (memo shared per CTA)
+    for (;;) {
+      if (tid == 0) sm.cur_item = (long long)atomicAdd(jb.queue, 1ull);
+      __syncthreads();
+      const long long item = sm.cur_item;
+      __syncthreads();
+      if (item >= jb.n_items) break;
+      s.evaluate_frac_item(jb.frac_items[item], jb.frac_out + item);
+      if (tid == 0 && sm.status && jb.status_out) atomicCAS(jb.status_out, 0, sm.status);
+    }
+    return;
+  }
   if (jb.kind == JOB_SWEEP) {
     for (;;) {
       if (tid == 0) sm.cur_item = (long long)atomicAdd(jb.queue, 1ull);

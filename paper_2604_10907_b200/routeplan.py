@@ -623,6 +623,24 @@ class Engine:
         self._chk(self.L.rw_sweep_slo_async(self.h, S, lptr(ids), iptr(pi), len(t), dptr(t),
                                             C.byref(oc), bps, shard_rank, shard_count))
 
+    def sweep_spec(self, profile_index, setup_ids, taus, opt: OptimizeContext, params,
+                   depth: int = 2):
+        """rw_sweep_spec: the sweep with a speculative beta bisection (depth levels/round)."""
+        pi = np.ascontiguousarray(profile_index, np.int32).reshape(-1)
+        S = len(pi) // max(self.m, 1)
+        ids = np.ascontiguousarray(setup_ids if setup_ids is not None else np.arange(S),
+                                   np.int64)
+        t = np.ascontiguousarray(taus, np.float64)
+        plist = params if isinstance(params, (list, tuple)) else [params] * len(t)
+        bps = (_abi.rw_beta_params * len(t))(*[q.c() for q in plist])
+        recs = np.zeros(max(S * len(t), 1), dtype=_abi.RECORD_DTYPE)
+        n_out = C.c_int64()
+        oc = opt.c()
+        self._chk(self.L.rw_sweep_spec(self.h, S, lptr(ids), iptr(pi), len(t), dptr(t),
+                                       C.byref(oc), bps, depth, C.c_void_p(recs.ctypes.data),
+                                       C.byref(n_out)))
+        return recs[: S * len(t)]
+
     def set_records_device(self, ptr: int, cap_records: int):
         """Sweeps write their records into this caller-owned device buffer (0 = ctx-owned)."""
         self._chk(self.L.rw_set_records_device(self.h, C.c_void_p(ptr or None),

@@ -318,3 +318,28 @@ def test_binary_file_and_pinned_async_load_give_identical_sweeps(eng, tmp_path):
         eng.load_profiles(inp.koff, inp.kx, inp.ky)
         out.append(eng.sweep(inp.profile_index, inp.retained, opt, bp))
     assert out[0].tobytes() == out[1].tobytes()
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_speculative_bisection_records_identical(eng, depth):
+    """f4: rw_sweep_spec evaluates `depth` levels of each instance's beta-bisection tree per
+    launch and follows the realised path on the host (routing_opt.cpp:154-171) — every
+    record field equals the sequential sweep's, bit for bit, except exec_passes (which also
+    counts the discarded speculative branches)."""
+    cfg = wl.config("C1", n=3000)
+    inp = wl.build_inputs(cfg)
+    s = wl.scores_for(cfg)
+    eng.load_scores(s)
+    eng.load_profiles(inp.koff, inp.kx, inp.ky)
+    taus = [90.0, 120.0]
+    params = [wl.with_span_epsilon(wl.truncated_params(), t, 16.0) for t in taus]
+    opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=taus[0], kappa=cfg.kappa)
+    seq = eng.sweep_slo(inp.profile_index, inp.retained, taus, opt, params)
+    spec = eng.sweep_spec(inp.profile_index, inp.retained, taus, opt, params, depth=depth)
+    assert len(seq) == len(spec) == 128
+    for f in seq.dtype.names:
+        if f == "exec_passes":
+            assert (spec[f] > 0).all()  # memo hits depend on which CTA ran what
+            continue
+        assert np.array_equal(seq[f].view(np.uint8), spec[f].view(np.uint8)), f
+    assert (seq["bisect_steps"] >= 3).all()  # span/16: a real bisection
