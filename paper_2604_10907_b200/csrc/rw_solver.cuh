@@ -694,13 +694,27 @@ struct Solver {
 
   // 2-D tiled TMA: SR rows x M doubles at row r0 into a stage, swizzled (see rd2).  Rows
   // past N are zero-filled and still counted in the transaction bytes (the full box).
-  __device__ __forceinline__ void tma_load_rows(void* dst, int r0, unsigned long long* bar) const {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  // Shared-space addresses (u32) and the descriptor's address are computed once per sweep
+  // by the caller: per-stage generic->shared conversions were 5 % of the pass's instructions.
+  __device__ __forceinline__ static void tma_load_rows(unsigned d, unsigned long long tmap,
+                                                       int r0, unsigned b) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(d),
-        "l"(reinterpret_cast<unsigned long long>(&jb.tmap)), "r"(0), "r"(r0), "r"(b)
+        "l"(tmap), "r"(0), "r"(r0), "r"(b)
+        : "memory");
+  }
+  __device__ __forceinline__ static void mbar_expect_tx_s(unsigned b, unsigned bytes) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(b),
+                 "r"(bytes)
+                 : "memory");
+  }
+  __device__ __forceinline__ static void mbar_wait_s(unsigned a, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(a),
+        "r"(parity), "r"(0x989680)
         : "memory");
   }
   // Full-width rows of 32/64/128 bytes come in through the tensor map with the matching
@@ -709,27 +723,36 @@ struct Solver {
   // hit 8 different bank groups (row-major stages are 2/4/8-way bank-conflicted).
   static constexpr bool SWZ = (MM == 4 || MM == 8 || MM == 16);
   static constexpr unsigned SWZ_MASK = (MM == 4) ? 1u : ((MM == 8) ? 3u : 7u);
+  // 16-byte chunk q of stage row r: an LDS.128 from the stage's shared-space address.
   template <bool FULLM>
-  __device__ __forceinline__ static double2 rd2(const unsigned char* stg, int r, int q, int m_) {
+  __device__ __forceinline__ static double2 rd2(unsigned stg, int r, int q, int m_) {
+    unsigned off;
     if constexpr (FULLM && SWZ) {
-      const unsigned off = (unsigned)r * (MM * 8) + (unsigned)q * 16u;
-      return *reinterpret_cast<const double2*>(stg + (off ^ (((off >> 7) & SWZ_MASK) << 4)));
+      off = (unsigned)r * (MM * 8) + (unsigned)q * 16u;
+      off ^= ((off >> 7) & SWZ_MASK) << 4;
     } else {
-      return reinterpret_cast<const double2*>(stg + (size_t)r * m_ * 8)[q];
+      off = (unsigned)(r * m_ * 8) + (unsigned)q * 16u;
     }
+    double2 x;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x.x), "=d"(x.y) : "r"(stg + off));
+    return x;
   }
-  // One ring stage of SR rows starting at r0 (lane 0 issues).
+  // One ring stage of SR rows starting at r0 into the stage at shared address dst with
+  // completion on the mbarrier at shared address bar (lane 0 issues).
   template <bool FULLM>
-  __device__ __forceinline__ void issue_stage(unsigned char* dst, int r0, int n_, int m_,
-                                              unsigned long long* bar) const {
+  __device__ __forceinline__ void issue_stage(unsigned dst, unsigned long long tmap, int r0,
+                                              int n_, int m_, unsigned bar) const {
     if (FULLM && SWZ) {
-      mbar_expect_tx(bar, (unsigned)SM::STAGE_BYTES);
-      tma_load_rows(dst, r0, bar);
+      mbar_expect_tx_s(bar, (unsigned)SM::STAGE_BYTES);
+      tma_load_rows(dst, tmap, r0, bar);
     } else {
       const int nv = min(SM::SR, n_ - r0);
       const unsigned bytes = (unsigned)(nv * m_ * 8);
-      mbar_expect_tx(bar, bytes);
-      tma_load_1d(dst, jb.scores + (size_t)r0 * m_, bytes, bar);
+      mbar_expect_tx_s(bar, bytes);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(jb.scores + (size_t)r0 * m_), "r"(bytes), "r"(bar)
+          : "memory");
     }
   }
 
@@ -775,11 +798,15 @@ struct Solver {
     auto stage_row = [&](const int t) { return (t / NSTG) * TILE + wid_ * BLK + (t % NSTG) * SR; };
     const unsigned gbase = SMX.stg_cnt[wid_];  // stage t is this warp's stage gbase + t
     unsigned used = 0;
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(SMX.ring[wid_][0]);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(&SMX.stage_bar[wid_][0]);
+    const unsigned long long tmap = reinterpret_cast<unsigned long long>(&jb.tmap);
     auto issue = [&](const int t) {  // no-op past the last row
       const int r0 = stage_row(t);
       const unsigned g = gbase + (unsigned)t;
       if (lane_ == 0 && r0 < n_)
-        issue_stage<FULLM>(SMX.ring[wid_][g & 1], r0, n_, m_, &SMX.stage_bar[wid_][g & 1]);
+        issue_stage<FULLM>(ring_s + (g & 1) * SM::STAGE_BYTES, tmap, r0, n_, m_,
+                           bar_s + (g & 1) * 8u);
     };
     if (tma) issue(0);
     for (int k = 0; k < ntiles; ++k) {
@@ -806,16 +833,27 @@ struct Solver {
         double bj;
         int arg = 0;
         if (MODE == PASS_EVAL) {
-          bj = __dsub_rn(v[0], a[0]);
+          // priced argmax as a tree (depth log2 M instead of M - 1): a right group replaces
+          // the left one only when strictly greater, so ties keep the lowest index — the
+          // first maximum of the reference's scan (score_dual.cpp:35-43), same value
+          double xv[MM];
+          int ix[MM];
 #pragma unroll
-          for (int i = 1; i < MM; ++i) {
-            if (FULLM || i < m_) {
-              const double x = __dsub_rn(v[i], a[i]);
-              const bool gt = x > bj;
-              bj = gt ? x : bj;
-              arg = gt ? i : arg;
+          for (int i = 0; i < MM; ++i) {
+            xv[i] = (FULLM || i < m_) ? __dsub_rn(v[i], a[i]) : -CUDART_INF;
+            ix[i] = i;
+          }
+#pragma unroll
+          for (int st2 = 1; st2 < MM; st2 <<= 1) {
+#pragma unroll
+            for (int i = 0; i + st2 < MM; i += 2 * st2) {
+              const bool gt = xv[i + st2] > xv[i];
+              xv[i] = gt ? xv[i + st2] : xv[i];
+              ix[i] = gt ? ix[i + st2] : ix[i];
             }
           }
+          bj = xv[0];
+          arg = ix[0];
         } else {
           arg = (mo_in && valid) ? (int)mo_in[j] : 0;
           bj = v[arg];
@@ -826,12 +864,12 @@ struct Solver {
         sb += bj;
         neg |= bj < 0.0;
         const bool cnt = valid && want_counts;
+        const unsigned long long inc = cnt ? (1ull << ((arg & 3) * 16)) : 0ull;
         if (NPK == 1) {
-          pk[0] += cnt ? (1ull << (arg * 16)) : 0ull;
+          pk[0] += inc;
         } else {
 #pragma unroll
-          for (int q = 0; q < NPK; ++q)
-            pk[q] += (cnt && (arg >> 2) == q) ? (1ull << ((arg & 3) * 16)) : 0ull;
+          for (int q = 0; q < NPK; ++q) pk[q] += ((arg >> 2) == q) ? inc : 0ull;
         }
         if (WMO && valid) mo_out[j] = (uint8_t)arg;
       };
@@ -842,9 +880,9 @@ struct Solver {
           if (stage_row(t) >= n_) break;  // never issued: rows past the end stay b = 0
           issue(t + 1);  // the other slot was released by the __syncwarp below
           const unsigned g = gbase + (unsigned)t;
-          mbar_wait(&SMX.stage_bar[wid_][g & 1], (g >> 1) & 1);
+          mbar_wait_s(bar_s + (g & 1) * 8u, (g >> 1) & 1);
           ++used;
-          const unsigned char* stg = SMX.ring[wid_][g & 1];
+          const unsigned stg = ring_s + (g & 1) * SM::STAGE_BYTES;
 #pragma unroll
           for (int i = 0; i < RL; ++i) {
             const int r = i * 32 + lane_;
@@ -1151,12 +1189,16 @@ struct Solver {
     constexpr int SR = SM::SR, RL = SM::RL;
     if (wid >= WP) return;
     const unsigned gbase = SMX.stg_cnt[wid];  // stage t is this warp's stage gbase + t
+    const unsigned ring_s = (unsigned)__cvta_generic_to_shared(SMX.ring[wid][0]);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(&SMX.stage_bar[wid][0]);
+    const unsigned long long tmap = reinterpret_cast<unsigned long long>(&jb.tmap);
     auto row0 = [&](const int t) { return (t * WP + wid) * SR; };
     auto issue = [&](const int t) {
       const int r0 = row0(t);
       const unsigned g = gbase + (unsigned)t;
       if (lane == 0 && r0 < n)
-        issue_stage<FULLM>(SMX.ring[wid][g & 1], r0, n, m_, &SMX.stage_bar[wid][g & 1]);
+        issue_stage<FULLM>(ring_s + (g & 1) * SM::STAGE_BYTES, tmap, r0, n, m_,
+                           bar_s + (g & 1) * 8u);
     };
     issue(0);
     int t = 0;
@@ -1164,8 +1206,8 @@ struct Solver {
     for (; row0(t) < n; ++t) {
       issue(t + 1);  // the other slot was released by the __syncwarp below
       const unsigned g = gbase + (unsigned)t;
-      mbar_wait(&SMX.stage_bar[wid][g & 1], (g >> 1) & 1);
-      const unsigned char* stg = SMX.ring[wid][g & 1];
+      mbar_wait_s(bar_s + (g & 1) * 8u, (g >> 1) & 1);
+      const unsigned stg = ring_s + (g & 1) * SM::STAGE_BYTES;
       const int r0 = row0(t);
 #pragma unroll
       for (int ii = 0; ii < RL; ++ii) {
