@@ -49,9 +49,15 @@ OUT = os.path.dirname(os.path.abspath(__file__))
 SPECS = {
     "C2": ("C2", None, 1, "truncated"),
     "C3": ("C3", None, 3, "truncated"),
-    "C5": ("C5", None, 2, "truncated"),
+    # C5's adversarial ties make the reference's repair_counts cost ~20 min per call at 1M
+    # rows (Phase 1: one full scan per single move, ~1.6e5 moves), so the C5 sample is the
+    # first 4 retained setups (models A-D at their first choice) and the per-setup
+    # restatement records (a second full run of the same algorithm) are skipped: the rows,
+    # the plan and the winner policy come from the reference itself.
+    "C5": ("C5", None, 4, "truncated"),
     "C1D": ("C1", 2000, 0, "default"),
 }
+NO_ORACLE = {"C5"}
 
 
 def hx(x):
@@ -140,8 +146,10 @@ def generate(name, threads):
             pol = dict(alpha=[hx(x) for x in d["alpha"]], score=hx(d["score"]),
                        dual_bound=hx(d["dual_bound"]), counts=[int(x) for x in counts],
                        assignment_sha256=sha(d["assignment"].astype(np.int32)))
-        with Pool(threads, initializer=_init, initargs=(name,)) as pool:
-            orc = pool.map(_oracle_record, [(k, tau, schedule) for k in range(S)])
+        orc = None
+        if name not in NO_ORACLE:
+            with Pool(threads, initializer=_init, initargs=(name,)) as pool:
+                orc = pool.map(_oracle_record, [(k, tau, schedule) for k in range(S)])
         win = None
         for k in range(S):  # the plan's setup among the sweep rows
             if ref["feasible"] and hx(ref["sweep_score"][k]) == hx(ref["score"]) and \

@@ -341,5 +341,5 @@ def test_speculative_bisection_records_identical(eng, depth):
         if f == "exec_passes":
             assert (spec[f] > 0).all()  # memo hits depend on which CTA ran what
             continue
-        assert np.array_equal(seq[f].view(np.uint8), spec[f].view(np.uint8)), f
+        assert np.ascontiguousarray(seq[f]).tobytes() == np.ascontiguousarray(spec[f]).tobytes(), f
     assert (seq["bisect_steps"] >= 3).all()  # span/16: a real bisection

@@ -74,17 +74,20 @@ def test_protocol_vs_reference(eng, name):
     for ti, sl in enumerate(g["slos"]):
         part = recs[ti * S:(ti + 1) * S]
         for k in range(S):
-            r, ref, orc = part[k], sl["sweep"][k], sl["oracle"][k]
+            r, ref = part[k], sl["sweep"][k]
             assert int(r["setup_id"]) == ref["id"] and int(r["status"]) == 0
             assert bool(r["feasible"]) == ref["feasible"], (name, sl["tau"], k)
             assert bits(r["score"]) == hb(ref["score"]), (name, sl["tau"], k)
             assert bits(r["latency_ms"]) == hb(ref["latency_ms"]), (name, sl["tau"], k)
+            assert 0 < int(r["exec_passes"]) <= int(r["eval_passes"])
+            if sl["oracle"] is None:  # C5: rows, plan and policy from the reference only
+                continue
+            orc = sl["oracle"][k]
             assert bits(r["beta"]) == hb(orc["beta"]), (name, sl["tau"], k)
             assert np.array_equal(bits(r["w"][:m]), [hb(x) for x in orc["w"]]), (name, k)
             assert int(r["eval_passes"]) == orc["eval_passes"], (name, sl["tau"], k)
             assert int(r["polish_passes"]) == orc["polish_passes"], (name, sl["tau"], k)
             assert int(r["repair_calls"]) == orc["repair_calls"], (name, sl["tau"], k)
-            assert 0 < int(r["exec_passes"]) <= int(r["eval_passes"])
         win = rw.reduce_records(part)
         plan = sl["plan"]
         assert (win if win >= 0 else None) == plan["winner"], (name, sl["tau"])
