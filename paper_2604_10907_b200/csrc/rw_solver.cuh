@@ -820,9 +820,9 @@ struct Solver {
       const bool pred_ok = in_binade(P + (double)wid_ * blk_est, 0.0, e_pred, ng_pred);
       const double scale =
           pred_ok ? __longlong_as_double((long long)(52 - e_pred + 1023) << 52) : 1.0;
-      long long Q = 0;
+      long long Q = 0, Q1 = 0;
       bool tie = false, neg = false;
-      double sb = 0.0, sa = 0.0;
+      double sb = 0.0, sb1 = 0.0, sa = 0.0;
       const long long t0 = prof ? clock64() : 0;
       // -- loads + priced argmax + speculative quanta -----------------------------------
       // branch-free (rows past the end compute on stale ring bytes and are then zeroed):
@@ -860,8 +860,15 @@ struct Solver {
         }
         bj = valid ? bj : 0.0;
         scr[g * 32 + lane_] = bj;
-        Q += quanta(bj, scale, tie);
-        sb += bj;
+        // two partial sums by row parity (shorter dependency chains; the integer sum is
+        // exact in any order, the approximate one is covered by the margin in any order)
+        if (g & 1) {
+          Q1 += quanta(bj, scale, tie);
+          sb1 += bj;
+        } else {
+          Q += quanta(bj, scale, tie);
+          sb += bj;
+        }
         neg |= bj < 0.0;
         const bool cnt = valid && want_counts;
         const unsigned long long inc = cnt ? (1ull << ((arg & 3) * 16)) : 0ull;
@@ -985,7 +992,8 @@ struct Solver {
       // sum |b| for the margins: equal to sum b when no b is negative (same operands, same
       // order) — the common case once the prices are gauged; otherwise from the smem copy
       // (any order: the margin covers every summation order)
-      sb = warp_sum_d(sb);
+      Q += Q1;
+      sb = warp_sum_d(sb + sb1);
       if (__any_sync(FULL, neg)) {
         double t = 0.0;
 #pragma unroll
@@ -1225,15 +1233,21 @@ struct Solver {
           }
         }
         if (MM & 1) v[MM - 1] = 0.0;
-        double rest = -CUDART_INF, vi = 0.0;
+        // max_{q != i}(s_q - a_q) as a tree (depth log2 M; max is exact in any order)
+        double xr[MM];
+        double vi = 0.0;
 #pragma unroll
         for (int q = 0; q < MM; ++q) {
-          if (FULLM || q < m_) {
-            if (q == i) vi = v[q];
-            else rest = smax(rest, __dsub_rn(v[q], a[q]));
-          }
+          const bool use = (FULLM || q < m_) && q != i;
+          if (q == i) vi = v[q];
+          xr[q] = use ? __dsub_rn(v[q], a[q]) : -CUDART_INF;
         }
-        f(r0 + r < n, __dsub_rn(vi, rest));  // rows past the end: zero / stale, masked
+#pragma unroll
+        for (int st2 = 1; st2 < MM; st2 <<= 1) {
+#pragma unroll
+          for (int q = 0; q + st2 < MM; q += 2 * st2) xr[q] = smax(xr[q], xr[q + st2]);
+        }
+        f(r0 + r < n, __dsub_rn(vi, xr[0]));  // rows past the end: zero / stale, masked
       }
       __syncwarp();  // every lane is done with this slot before it is refilled
     }
