@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--schedule", default="truncated", choices=["truncated", "default"])
-    ap.add_argument("--n", type=int, default=None, help="override prompt count (debug)")
+    ap.add_argument("--prompts", type=int, default=None, help="override prompt count (debug)")
     ap.add_argument("--setups", type=int, default=None, help="limit retained setups (debug)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -271,7 +271,7 @@ def reference_arm(args):
     from oracle import Reference
     from paper_2604_10907_b200 import workloads as wl  # pure-Python workload description
     R = Reference()
-    cfg = wl.config(args.workload, args.n)
+    cfg = wl.config(args.workload, args.prompts)
     # inputs from the reference library's own producers: nothing of ours is loaded
     inp = wl.build_inputs(cfg, limit=args.setups, enumerate_fn=R.enumerate_retain)
     s = wl.scores_for(cfg, synth=R.synth_scores)
@@ -346,7 +346,7 @@ def main():
     from paper_2604_10907_b200 import shard
     from paper_2604_10907_b200 import workloads as wl
 
-    cfg = wl.config(args.workload, args.n)
+    cfg = wl.config(args.workload, args.prompts)
     inp = wl.build_inputs(cfg, limit=args.setups)
     s_host = wl.scores_for(cfg)
     taus = np.array(cfg.taus, np.float64)  # strong scaling: the same sweep at every N
@@ -357,7 +357,12 @@ def main():
     sample = sample_spec(cfg)
 
     eng = rw.Engine(local)
-    stream = torch.cuda.current_stream(dev)
+    # ONE stream for everything of the step — the L2 flush, the record-buffer reset, the
+    # sweep kernel, the NCCL gather and the timing events — so they are ordered.  (torch's
+    # default stream is the legacy NULL stream, handle 0, which rw_set_stream reads as "the
+    # context's own stream": the reset could then overlap the kernel's record writes.)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     scores_dev = torch.from_numpy(s_host).to(dev)
     eng.bind_scores_device(scores_dev.data_ptr(), cfg.n, cfg.m)
@@ -373,7 +378,11 @@ def main():
         if world > 1 and not shared:
             allrec = shard.gather_device_records(recbuf)
         elif world > 1:
-            allrec = shard.gather_records(eng.sweep_fetch(), n_inst)
+            mine = eng.sweep_fetch()
+            if os.environ.get("RW_BENCH_DEBUG"):
+                print(f"rank {rank}: {len(mine)} records, {int((mine['setup_id'] >= 0).sum())} valid",
+                      file=sys.stderr, flush=True)
+            allrec = shard.gather_records(mine, n_inst)
         else:
             allrec = eng.sweep_fetch()
         return allrec, shard.winners_per_slo(allrec, [float(t) for t in taus])

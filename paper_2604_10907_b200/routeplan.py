@@ -439,6 +439,9 @@ class Engine:
 
     # inputs ---------------------------------------------------------------------------
     def set_stream(self, stream_handle: int):
+        """Launch on this cudaStream_t.  0 selects the context's own stream (NOT the legacy
+        default stream — pass 1, cudaStreamLegacy, for that); torch's default stream has
+        handle 0, so share a torch.cuda.Stream() with the engine to order work."""
         self._chk(self.L.rw_set_stream(self.h, C.c_void_p(stream_handle)))
 
     def load_scores(self, scores: np.ndarray):
