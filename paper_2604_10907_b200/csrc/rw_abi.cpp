@@ -153,7 +153,7 @@ int ensure_ws(rw_ctx* ctx, int slots) {
   if (ctx->d_mo) cudaFree(ctx->d_mo);
   ctx->d_mo = nullptr;
   ctx->ws_entries = 0;
-  CK(cudaMalloc(&ctx->d_mo, std::max<size_t>(need, 1)));
+  CK(cudaMalloc(&ctx->d_mo, std::max<size_t>(need, 1) + 64));  // +64: 16-byte tail loads
   ctx->ws_entries = need;
   return RW_OK;
 }

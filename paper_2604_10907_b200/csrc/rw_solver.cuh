@@ -103,6 +103,7 @@ enum Prof {
   PR_REFCYC = 25,    // repair Phase 2 list refreshes (cycles)
   PR_P2SEED = 26,    // repair Phase 2 seeding sweep (cycles)
   PR_PHIST = 27,     // polish: overfull shells resolved by the value-bin histogram sweep
+  PR_P2MERGE = 29,   // repair Phase 2: parallel joined-list folds
 };
 struct Piece {
   long long q;
@@ -2087,8 +2088,8 @@ struct Solver {
   // Where the lists live.  The TMA ring is idle during repair Phase 2 (its sweeps use plain
   // loads), so for small M the lists sit in it — every bookkeeping access of the serial
   // cycle loop is then a shared-memory access; larger M use this CTA's global slot.
-  static constexpr int PH2_EC_SMEM = 16;
-  __device__ Ph2 ph2_ws() const {
+  static constexpr int PH2_EC_SMEM = 64;
+  __device__ Ph2 ph2_ws(bool global_lists = false) const {
     const size_t P = (size_t)m * m;
     const size_t ring = sizeof(SMX.ring);
     const long long ksm =
@@ -2096,7 +2097,7 @@ struct Solver {
         ((long long)P * 12);
     Ph2 w;
     unsigned char* b;
-    if (ksm >= 32) {
+    if (ksm >= 32 && !global_lists) {
       b = &SMX.ring[0][0][0];
       w.K = (int)min(ksm, (long long)P1BUF);
       w.EC = PH2_EC_SMEM;
@@ -2110,6 +2111,16 @@ struct Solver {
     w.Lj = reinterpret_cast<int*>(w.Eg + P * w.EC);
     w.Ej = w.Lj + P * w.K;
     w.h = reinterpret_cast<Ph2Hdr*>(w.Ej + P * w.EC);
+    // long lists in global memory: the small, hot parts (joined lists, headers) in the idle
+    // ring when they fit — the serial move loop shifts joined-list entries on every move
+    const size_t hot = P * (PH2_EC_SMEM * 12 + sizeof(Ph2Hdr));
+    if (b != &SMX.ring[0][0][0] && hot <= ring) {
+      unsigned char* r = &SMX.ring[0][0][0];
+      w.EC = PH2_EC_SMEM;
+      w.Eg = reinterpret_cast<double*>(r);
+      w.Ej = reinterpret_cast<int*>(w.Eg + P * w.EC);
+      w.h = reinterpret_cast<Ph2Hdr*>(w.Ej + P * w.EC);
+    }
     return w;
   }
   // Warp 0 (one lane per pair): gain / witness of every pair from the list heads into
@@ -2158,6 +2169,88 @@ struct Solver {
     for (int off = 16; off > 0; off >>= 1) need = min(need, __shfl_xor_sync(FULL, need, off));
     if (lane == 0) SMX.flag = (need == 0x7fffffff) ? -1 : need;
   }
+  // CTA: the same fold (see ph2_merge) in parallel — every entry's position in the merged
+  // list is its index plus the number of entries of the other list ranking before it (a
+  // binary search; an E entry ranks before an identical L entry), all reads before one
+  // barrier, all writes after it.  Run between passes for pairs whose E is nearly full.
+  __device__ void ph2_merge_par(Ph2& w, int p) {
+    __syncthreads();
+    Ph2Hdr& h = w.h[p];
+    const int head = h.head, len = h.len, eh = h.ehead, el = h.elen;
+    const bool complete = h.complete != 0;
+    double* Lg = w.Lg + (size_t)p * w.K;
+    int* Lj = w.Lj + (size_t)p * w.K;
+    const double* Eg = w.Eg + (size_t)p * w.EC;
+    const int* Ej = w.Ej + (size_t)p * w.EC;
+    const bool have_tail = len > 0;
+    const double tg = have_tail ? Lg[len - 1] : 0.0;
+    const int tj = have_tail ? Lj[len - 1] : 0;
+    int eb = el;  // E's usable prefix (ranks before the refresh tail) when L is incomplete
+    if (!complete)
+      while (eb > eh && !(have_tail && (Eg[eb - 1] > tg || (Eg[eb - 1] == tg && Ej[eb - 1] < tj))))
+        --eb;
+    const int nl = len - head, ne = eb - eh;
+    const int total = min(w.K, nl + ne);
+    const bool newc = complete && eb == el && nl + ne <= w.K;
+    constexpr int PER = (P1BUF + T - 1) / T;
+    double lg[PER];
+    int lj[PER], lpos[PER];
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = tid + r * T;
+      lpos[r] = 0x7fffffff;
+      if (i < nl) {
+        lg[r] = Lg[head + i];
+        lj[r] = Lj[head + i];
+        int lo = 0, hi = ne;  // E entries ranking before (lg, lj): (g > lg) or (g == lg, j <= lj)
+        while (lo < hi) {
+          const int md = (lo + hi) >> 1;
+          const double g = Eg[eh + md];
+          const int j = Ej[eh + md];
+          if (g > lg[r] || (g == lg[r] && j <= lj[r])) lo = md + 1;
+          else hi = md;
+        }
+        lpos[r] = i + lo;
+      }
+    }
+    double eg = 0.0;
+    int ej = 0, epos = 0x7fffffff;
+    if (tid < ne) {
+      eg = Eg[eh + tid];
+      ej = Ej[eh + tid];
+      int lo = 0, hi = nl;  // L entries ranking strictly before (eg, ej)
+      while (lo < hi) {
+        const int md = (lo + hi) >> 1;
+        const double g = Lg[head + md];
+        const int j = Lj[head + md];
+        if (g > eg || (g == eg && j < ej)) lo = md + 1;
+        else hi = md;
+      }
+      epos = tid + lo;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; ++r)
+      if (lpos[r] < total) {
+        Lg[lpos[r]] = lg[r];
+        Lj[lpos[r]] = lj[r];
+      }
+    if (epos < total) {
+      Lg[epos] = eg;
+      Lj[epos] = ej;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      h.head = 0;
+      h.len = total;
+      h.complete = newc;
+      h.ehead = h.elen = 0;
+      if (!newc && total == 0) h.need = 1;
+      SMX.prof[PR_P2MERGE]++;
+    }
+    __syncthreads();
+  }
+
   // Thread 0: fold pair p's joined list E into its best-member list L (both sorted by
   // (gain desc, j asc)), keeping at most K entries.  Invariant of an incomplete L: every
   // member of u in neither list ranks after L's tail (its last entry at the refresh, dead or
@@ -2259,11 +2352,28 @@ struct Solver {
     int u, v;
     template <class F>
     __device__ __forceinline__ void operator()(F& f) {
-      const int m_ = s->m;
-      for (int j = s->tid; j < s->n; j += T) {
-        if (s->mo[j] != u) continue;
-        const double* row = s->jb.scores + (size_t)j * m_;
-        f(dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))), j, v);
+      const int m_ = s->m, n_ = s->n;
+      const uint8_t* mo_ = s->mo;
+      const bool vec = ((reinterpret_cast<uintptr_t>(mo_) & 15u) == 0);
+      for (int b0 = s->tid * 16; b0 < n_; b0 += T * 16) {  // 16 rows of model_of per load
+        uint4 w4;
+        if (vec) {
+          w4 = *reinterpret_cast<const uint4*>(mo_ + b0);
+        } else {
+          unsigned char t[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) t[q] = (b0 + q < n_) ? mo_[b0 + q] : 0xff;
+          memcpy(&w4, t, 16);
+        }
+        const unsigned wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int j = b0 + q;
+          if (j < n_ && ((wd[q >> 2] >> (8 * (q & 3))) & 0xffu) == (unsigned)u) {
+            const double* row = s->jb.scores + (size_t)j * m_;
+            f(dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))), j, v);
+          }
+        }
       }
     }
   };
@@ -2276,11 +2386,29 @@ struct Solver {
   __device__ void ph2_refresh(Ph2& w, int u, int v) {
     const int p = u * m + v;
     unsigned long long kmin = ~0ull;
-    for (int j = tid; j < n; j += T) {
-      if (mo[j] != u) continue;
-      const double* row = jb.scores + (size_t)j * m;
-      const unsigned long long key = dkey(__dsub_rn(__ldg(row + u), __ldg(row + v)));
-      kmin = key < kmin ? key : kmin;
+    // model_of is scanned 16 rows per thread-iteration (one 16-byte load; the workspace is
+    // padded so the tail load stays inside it)
+    const bool vec = ((reinterpret_cast<uintptr_t>(mo) & 15u) == 0);
+    for (int b0 = tid * 16; b0 < n; b0 += T * 16) {
+      uint4 w4;
+      if (vec) {
+        w4 = *reinterpret_cast<const uint4*>(mo + b0);
+      } else {
+        unsigned char t[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) t[q] = (b0 + q < n) ? mo[b0 + q] : 0xff;
+        memcpy(&w4, t, 16);
+      }
+      const unsigned wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int j = b0 + q;
+        if (j < n && ((wd[q >> 2] >> (8 * (q & 3))) & 0xffu) == (unsigned)u) {
+          const double* row = jb.scores + (size_t)j * m;
+          const unsigned long long key = dkey(__dsub_rn(__ldg(row + u), __ldg(row + v)));
+          kmin = key < kmin ? key : kmin;
+        }
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -2294,20 +2422,34 @@ struct Solver {
     __syncthreads();
     for (int w2 = 0; w2 < W; ++w2) kmin = kred[w2] < kmin ? kred[w2] : kmin;
     // members with key == kmin in increasing j, the first K (chunks of R rows per thread)
-    constexpr int R = 4;
+    constexpr int R = 16;
     int got = 0;
     for (int base = 0; base < n && got < w.K; base += T * R) {
-      int hit[R];
+      unsigned hitm = 0;
       int c = 0;
+      {
+        const int b0 = base + tid * R;
+        uint4 w4 = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+        if (vec && b0 < n) {
+          w4 = *reinterpret_cast<const uint4*>(mo + b0);
+        } else if (b0 < n) {
+          unsigned char t[16];
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int j = base + tid * R + q;
-        hit[q] = 0;
-        if (j < n && mo[j] == u) {
-          const double* row = jb.scores + (size_t)j * m;
-          hit[q] = dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))) == kmin;
+          for (int q = 0; q < 16; ++q) t[q] = (b0 + q < n) ? mo[b0 + q] : 0xff;
+          memcpy(&w4, t, 16);
         }
-        c += hit[q];
+        const unsigned wd[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int j = b0 + q;
+          if (j < n && ((wd[q >> 2] >> (8 * (q & 3))) & 0xffu) == (unsigned)u) {
+            const double* row = jb.scores + (size_t)j * m;
+            if (dkey(__dsub_rn(__ldg(row + u), __ldg(row + v))) == kmin) {
+              hitm |= 1u << q;
+              ++c;
+            }
+          }
+        }
       }
       int incl = c;  // block exclusive prefix of c in thread (= row) order
 #pragma unroll
@@ -2325,7 +2467,7 @@ struct Solver {
       int pos = before + incl - c;
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        if (hit[q]) {
+        if ((hitm >> q) & 1u) {
           if (pos < w.K) {
             SMX.cand[2 * pos] = kmin;
             SMX.cand[2 * pos + 1] = ((unsigned long long)(unsigned)(base + tid * R + q) << 8) |
@@ -2360,6 +2502,108 @@ struct Solver {
     __syncthreads();
   }
 
+  // ---- repair Phase 1 from the pair lists (tie-heavy data) -------------------------------
+  // The reference's Phase 1 takes, one move at a time, the global minimum of
+  // (loss = s_ju - s_jv, j, v) over prompts j of a surplus model u and deficit models v
+  // (score_dual.cpp:96-118).  Moved prompts land in deficit models, which never become
+  // surplus, so every pair's candidates only leave: pair (u, v)'s best-member list (the same
+  // ordering as Phase 2's: key(s_ju - s_jv) asc, j asc) yields its candidates in order, and the
+  // global minimum is the minimum of the active pairs' heads by (loss, j, v).  Thread 0 runs
+  // the move loop on cached heads (SMX.gain = head gain = -loss, SMX.witness = head j; -1 =
+  // pair exhausted, -2 = list dry before all members were seen -> refresh); a move only
+  // re-validates the pairs whose head was the moved prompt.  Lists live in the global slot
+  // (K ~ 1300 for M = 8): ~10^5 moves need ~10^2 refreshes instead of ~10^2 threshold sweeps
+  // per 2048 moves.
+  __device__ void ph1_head(Ph2& w, int p) {  // thread 0: cache pair p's live head
+    const int u = p / m;
+    Ph2Hdr& h = w.h[p];
+    const int* Lj = w.Lj + (size_t)p * w.K;
+    while (h.head < h.len && mo[Lj[h.head]] != u) ++h.head;
+    if (h.head < h.len) {
+      SMX.witness[p] = Lj[h.head];
+      SMX.gain[p] = w.Lg[(size_t)p * w.K + h.head];
+    } else {
+      SMX.witness[p] = h.complete ? -1 : -2;
+    }
+  }
+  __device__ void phase1_lists() {
+    Ph2 w = ph2_ws(true);
+    if (tid == 0)
+      for (int p = 0; p < m * m; ++p) {
+        Ph2Hdr& h = w.h[p];
+        h.head = h.len = h.complete = h.ehead = h.elen = 0;
+        h.need = 1;
+        SMX.witness[p] = -2;
+      }
+    __syncthreads();
+    for (;;) {
+      // refresh every active pair whose list is unknown or dry
+      if (tid == 0) {
+        int need = -1;
+        for (int u = 0; u < m && need < 0; ++u)
+          for (int v = 0; v < m; ++v)
+            if (u != v && SMX.delta[u] > 0 && SMX.delta[v] < 0 && SMX.witness[u * m + v] == -2) {
+              need = u * m + v;
+              break;
+            }
+        SMX.flag = need;
+      }
+      __syncthreads();
+      const int pr = SMX.flag;
+      __syncthreads();
+      if (pr >= 0) {
+        const long long tr = clock64();
+        ph2_refresh(w, pr / m, pr % m);
+        if (tid == 0) {
+          ph1_head(w, pr);
+          SMX.prof[PR_REFCYC] += clock64() - tr;
+        }
+        __syncthreads();
+        continue;
+      }
+      // thread 0: moves in the reference's order until a list runs dry or no surplus is left
+      if (tid == 0) {
+        int state = 0;  // 0: done, 1: refresh needed
+        for (;;) {
+          int bp = -1;
+          double bg = 0.0;
+          int bj = 0, bv = 0;
+          bool dry = false;
+          for (int u = 0; u < m; ++u) {
+            if (SMX.delta[u] <= 0) continue;
+            for (int v = 0; v < m; ++v) {
+              if (v == u || SMX.delta[v] >= 0) continue;
+              const int p = u * m + v;
+              const int j = SMX.witness[p];
+              if (j == -2) dry = true;
+              if (j < 0) continue;
+              const double g = SMX.gain[p];  // max gain == min loss
+              if (bp < 0 || g > bg || (g == bg && (j < bj || (j == bj && v < bv)))) {
+                bp = p;
+                bg = g;
+                bj = j;
+                bv = v;
+              }
+            }
+          }
+          if (dry) {  // an active pair's next candidate is unknown
+            state = 1;
+            break;
+          }
+          if (bp < 0) break;  // no surplus left (or nothing movable)
+          const int u = bp / m;
+          move_prompt(bj, bv);
+          for (int x = 0; x < m; ++x)  // heads that were the moved prompt
+            if (x != u && SMX.witness[u * m + x] == bj) ph1_head(w, u * m + x);
+        }
+        SMX.flag = state;
+      }
+      __syncthreads();
+      if (SMX.flag == 0) break;
+      __syncthreads();
+    }
+  }
+
   // ---- repair_counts (score_dual.cpp:81-185); counts in SMX.counts, targets in SMX.target
   __device__ double repair() {
     const long long t_rep = clock64();
@@ -2381,6 +2625,8 @@ struct Solver {
       if (surplus == 0) break;
       if (surplus <= 2) {
         phase1_single();
+      } else if (surplus > 4 * P1BUF) {  // long runs of moves (ties): pair lists
+        phase1_lists();
       } else {
         phase1_batch();
       }
@@ -2397,7 +2643,7 @@ struct Solver {
     if (tid == 0) SMX.prof[PR_P1CYC] += clock64() - tp1;
     if (m >= 2) {
       const long long tp2 = clock64();
-      Ph2 w = ph2_ws();
+      Ph2 w = ph2_ws(true);  // long lists: few refreshes (C5: 12k -> ~1k per 16 setups)
       phase2_gains();
       if (tid == 0) SMX.prof[PR_P2SEED] += clock64() - tp2;
       if (tid == 0) {
@@ -2431,34 +2677,59 @@ struct Solver {
           ph2_refresh(w, pr / m, pr % m);
           if (tid == 0) SMX.prof[PR_REFCYC] += clock64() - tr;
         }
-        if (tid == 0) {
+        // the best cycle in the reference's scan order (:142-167: all 2-cycles (u < v), then
+        // all 3-cycles (u, v, x); strict > against 1e-15 keeps the first maximum): warp 0
+        // splits the M^2 + M^3 candidates over lanes and reduces by (gain desc, order asc)
+        if (wid == 0) {
           double best = 1e-15;
+          int bo = 0x7fffffff;  // scan-order index of the best candidate
+          const int n2 = m * m, n3 = m * m * m;
+          for (int o = lane; o < n2 + n3; o += 32) {
+            double g;
+            bool ok;
+            if (o < n2) {
+              const int u = o / m, v = o % m;
+              ok = u < v;
+              g = ok ? __dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + u]) : 0.0;
+            } else {
+              const int t = o - n2, u = t / (m * m), v = (t / m) % m, x = t % m;
+              ok = v != u && x != u && x != v;
+              g = ok ? __dadd_rn(__dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + x]),
+                                 SMX.gain[x * m + u])
+                     : 0.0;
+            }
+            if (ok && g > best) {  // within a lane candidates come in scan order
+              best = g;
+              bo = o;
+            }
+          }
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) {
+            const double og = __shfl_xor_sync(FULL, best, off);
+            const int oo = __shfl_xor_sync(FULL, bo, off);
+            if (og > best || (og == best && oo < bo)) {
+              best = og;
+              bo = oo;
+            }
+          }
+          if (lane == 0) SMX.red_i[0] = bo;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          const int bo = SMX.red_i[0];
           int cu = -1, cv = -1, cw = -1;
-          for (int u = 0; u < m; ++u)
-            for (int v = u + 1; v < m; ++v) {
-              double g = __dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + u]);
-              if (g > best) {
-                best = g;
-                cu = u;
-                cv = v;
-                cw = -1;
-              }
+          if (bo != 0x7fffffff) {
+            const int n2 = m * m;
+            if (bo < n2) {
+              cu = bo / m;
+              cv = bo % m;
+            } else {
+              const int t = bo - n2;
+              cu = t / (m * m);
+              cv = (t / m) % m;
+              cw = t % m;
             }
-          for (int u = 0; u < m; ++u)
-            for (int v = 0; v < m; ++v) {
-              if (v == u) continue;
-              for (int x = 0; x < m; ++x) {
-                if (x == u || x == v) continue;
-                double g = __dadd_rn(__dadd_rn(SMX.gain[u * m + v], SMX.gain[v * m + x]),
-                                     SMX.gain[x * m + u]);
-                if (g > best) {
-                  best = g;
-                  cu = u;
-                  cv = v;
-                  cw = x;
-                }
-              }
-            }
+          }
           SMX.flag = (cu < 0);
           if (cu >= 0) {
             if (cw < 0) {
@@ -2476,6 +2747,13 @@ struct Solver {
         }
         __syncthreads();
         if (SMX.flag) break;
+        // fold nearly full joined lists into their best lists, in parallel (a pass files at
+        // most 3 prompts per pair, so E never overflows between these folds)
+        for (int pp = 0; pp < m * m; ++pp) {
+          if (pp / m == pp % m) continue;
+          const Ph2Hdr& hh = w.h[pp];
+          if (!hh.need && hh.elen - hh.ehead >= w.EC - 4) ph2_merge_par(w, pp);
+        }
         __syncthreads();
       }
       // the lists may have lived in the TMA ring: order these generic-proxy writes before
