@@ -52,6 +52,7 @@ struct rw_ctx {
   rw_setup_record* d_records_user = nullptr;  // caller-owned device buffer (optional)
   int64_t records_user_cap = 0;
   int64_t pending_records = -1;
+  std::vector<unsigned char> h_stage;  // pageable staging of per-sweep tables
   // speculative bisection (rw_sweep_spec)
   void* d_items = nullptr;
   size_t items_cap = 0;
@@ -751,19 +752,24 @@ int rw_sweep_slo_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
       return rc;
     ctx->d_setup_ids = static_cast<int64_t*>(p);
     ctx->setup_ids_cap = cap;
-    std::vector<int64_t> ids;
-    if (!setup_ids) {
-      ids.resize(n_setups);
+    // one pageable staging copy of the small per-sweep tables: a pageable-source
+    // cudaMemcpyAsync returns once the bytes are staged, so the call does not block on the
+    // stream (the next step's uploads overlap the running kernel) and the caller's arrays —
+    // even page-locked ones — may change as soon as this returns
+    std::vector<unsigned char>& st = ctx->h_stage;
+    const size_t b_ids = sizeof(int64_t) * n_setups, b_taus = sizeof(double) * n_slo,
+                 b_par = sizeof(rw_beta_params) * n_slo;
+    st.resize(b_ids + b_taus + b_par);
+    if (setup_ids) {
+      std::memcpy(st.data(), setup_ids, b_ids);
+    } else {
+      int64_t* ids = reinterpret_cast<int64_t*>(st.data());
       for (int64_t k = 0; k < n_setups; ++k) ids[k] = k;
-      setup_ids = ids.data();
     }
-    CK(cudaMemcpyAsync(ctx->d_setup_ids, setup_ids, sizeof(int64_t) * n_setups,
+    std::memcpy(st.data() + b_ids, taus, b_taus);
+    std::memcpy(st.data() + b_ids + b_taus, params, b_par);
+    CK(cudaMemcpyAsync(ctx->d_setup_ids, st.data(), b_ids + b_taus + b_par,
                        cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups, taus, sizeof(double) * n_slo,
-                       cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->d_setup_ids + n_setups + n_slo, params,
-                       sizeof(rw_beta_params) * n_slo, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));  // `ids` is stack-owned
   }
   if (ctx->d_records_user) {
     if (ctx->records_user_cap < items)
