@@ -28,12 +28,12 @@ ctas = min(len(recs), 296)
 cyc = ms * 1.965e6
 names = ["load(w0)", "totbar(w0)", "empty(w0)", "polish", "pmiss", "pradix", "walk_wait",
          "walk_busy", "fast_blocks", "slow_blocks", "raw_rows", "psweep", "pselect", "pass",
-         "repair", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell", "p_move", "p2_refresh", "p1_cyc", "p2_cyc", "ref_cyc", "p2_seed", "p_hist", "-", "p2_merge"]
+         "repair", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell", "p_move", "p2_refresh", "p1_cyc", "p2_cyc", "ref_cyc", "p2_seed", "p_hist", "-", "p2_merge", "p_fhit", "p_fused"]
 print(f"{which} x{len(recs)} ({sched}): kernel {ms:.3f} ms (~{cyc:.3e} cyc/CTA), eval passes {p}, "
       f"(reference trajectory {pref}), polish passes {pp}, evals/s {p * cfg.n / (ms / 1e3):.3e}")
 for i, nm in enumerate(names):
     v = pr[i]
-    if nm in ("pmiss", "pradix", "fast_blocks", "slow_blocks", "raw_rows", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell", "p2_refresh", "p_hist", "p2_merge"):
+    if nm in ("pmiss", "pradix", "fast_blocks", "slow_blocks", "raw_rows", "p1_rounds", "p2_passes", "moves", "p_over", "p_far", "p_shell", "p2_refresh", "p_hist", "p2_merge", "p_fhit"):
         print(f"  {nm:12s} {v:14d}  per pass {v / max(p, 1):10.2f}")
     elif nm == "p_move":
         ncoord = max(pp * cfg.m, 1)
