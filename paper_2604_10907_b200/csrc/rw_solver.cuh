@@ -1329,7 +1329,10 @@ struct Solver {
   }
 
   static constexpr int NSH = 3;  // nested windows a_i +- d * 8^s (value space)
-  static constexpr int PTARGET = 256;  // polish: keys aimed for inside the inner window
+#ifndef RW_PTARGET
+#define RW_PTARGET 128  // C3 probe sweep (profiles/r02_ptarget.txt): 64 21.07 s, 96 20.96, 128 21.02, 256 21.58, 512 21.31, 1024 21.45
+#endif
+  static constexpr int PTARGET = RW_PTARGET;  // polish: keys aimed for inside the inner window
   static_assert(2 * NSH <= 16, "red_i stride");
   struct CountWin {
     double lo[NSH], hi[NSH];
