@@ -235,7 +235,11 @@ int rw_sweep_slo(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                  const int32_t* profile_index, int32_t n_slo, const double* tau_ms,
                  const rw_opt_context* opt, const rw_beta_params* params, int32_t shard_rank,
                  int32_t shard_count, rw_setup_record* out_records, int64_t* n_out);
-/* Asynchronous variants: records stay in device memory (ctx-owned) until rw_sweep_fetch. */
+/* Asynchronous variants: enqueue the sweep on the ctx's stream and return without waiting
+ * for the device (the next step's uploads overlap the running kernel).  setup_ids, tau_ms
+ * and params are staged through a context-owned host buffer and may be reused at once;
+ * profile_index, when page-locked, must stay unchanged until rw_sweep_fetch.  Records stay
+ * in device memory (ctx-owned, or the rw_set_records_device buffer) until rw_sweep_fetch. */
 int rw_sweep_async(rw_ctx* ctx, int64_t n_setups, const int64_t* setup_ids,
                    const int32_t* profile_index, const rw_opt_context* opt,
                    const rw_beta_params* params, int32_t shard_rank, int32_t shard_count);

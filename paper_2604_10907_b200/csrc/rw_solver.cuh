@@ -2749,7 +2749,12 @@ struct Solver {
           }
         }
         __syncthreads();
-        if (SMX.flag) break;
+        // every thread reads the flag before thread 0 (or warp 0) can rewrite it for the
+        // next round: a late reader would otherwise leave the loop alone and desynchronise
+        // the CTA's barriers
+        const int brk1_ = SMX.flag;
+        __syncthreads();
+        if (brk1_) break;
         // fold nearly full joined lists into their best lists, in parallel (a pass files at
         // most 3 prompts per pair, so E never overflows between these folds)
         for (int pp = 0; pp < m * m; ++pp) {
@@ -2846,7 +2851,12 @@ struct Solver {
         }
       }
       __syncthreads();
-      if (SMX.flag) break;
+      // every thread reads the flag before thread 0 (or warp 0) can rewrite it for the
+      // next round: a late reader would otherwise leave the loop alone and desynchronise
+      // the CTA's barriers
+      const int brk2_ = SMX.flag;
+      __syncthreads();
+      if (brk2_) break;
     }
     if (tid == 0)
       for (int i = 0; i < m; ++i) SMX.polished[i] = SMX.best_alpha[i];
@@ -2862,7 +2872,12 @@ struct Solver {
         if (SMX.flag) SMX.converged = 1;
       }
       __syncthreads();
-      if (SMX.flag) break;
+      // every thread reads the flag before thread 0 (or warp 0) can rewrite it for the
+      // next round: a late reader would otherwise leave the loop alone and desynchronise
+      // the CTA's barriers
+      const int brk3_ = SMX.flag;
+      __syncthreads();
+      if (brk3_) break;
     }
     if (tid == 0) {  // gauge (:309-310)
       double lo = SMX.best_alpha[0];
@@ -2990,8 +3005,10 @@ struct Solver {
         }
       }
       __syncthreads();
-      if (SMX.status) return;
-      if (SMX.flag) break;
+      const int st_ = SMX.status, brk_f = SMX.flag;  // read before anyone rewrites them
+      __syncthreads();
+      if (st_) return;
+      if (brk_f) break;
     }
     if (tid == 0) {
       bool uniform = true;
