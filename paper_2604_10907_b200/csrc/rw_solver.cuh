@@ -1329,6 +1329,9 @@ struct Solver {
   }
 
   static constexpr int NSH = 3;  // nested windows a_i +- d * 8^s (value space)
+#ifndef RW_PSHELL
+#define RW_PSHELL 8  // ratio of the nested polish windows
+#endif
 #ifndef RW_PTARGET
 #define RW_PTARGET 128  // C3 probe sweep (profiles/r02_ptarget.txt): 64 21.07 s, 96 20.96, 128 21.02, 256 21.58, 512 21.31, 1024 21.45
 #endif
@@ -1512,7 +1515,7 @@ struct Solver {
       {
         double r = dl;
 #pragma unroll
-        for (int q = 0; q < NSH; ++q, r *= 8.0) {
+        for (int q = 0; q < NSH; ++q, r *= (double)RW_PSHELL) {
           cw.lo[q] = ai - r;
           cw.hi[q] = ai + r;
           cw.gt[q] = cw.lt[q] = 0;
