@@ -343,3 +343,32 @@ def test_speculative_bisection_records_identical(eng, depth):
             continue
         assert np.ascontiguousarray(seq[f]).tobytes() == np.ascontiguousarray(spec[f]).tobytes(), f
     assert (seq["bisect_steps"] >= 3).all()  # span/16: a real bisection
+
+
+def test_sweep_async_returns_before_the_kernel_and_stages_its_tables(eng):
+    """rw_sweep_slo_async enqueues the launch and returns without waiting for the device,
+    and the setup / SLO tables it was given may change as soon as it returns (they are
+    staged through a context-owned host buffer): the records equal the blocking sweep's."""
+    import time
+    cfg = wl.config("C2", n=100_000)
+    inp = wl.build_inputs(cfg, limit=64)
+    eng.load_scores(wl.scores_for(cfg))
+    eng.load_profiles(inp.koff, inp.kx, inp.ky)
+    tau = cfg.taus[0]
+    bp = wl.with_span_epsilon(wl.truncated_params(), tau, 4.0)
+    opt = rw.OptimizeContext(lambda_rps=cfg.lambda_rps, tau_ms=tau, kappa=cfg.kappa)
+    ref = eng.sweep(inp.profile_index, inp.retained, opt, bp)
+    kernel_ms = eng.last_kernel_ms()
+    t0 = time.perf_counter()
+    eng.sweep_async(inp.profile_index, inp.retained, opt, bp)
+    call_ms = (time.perf_counter() - t0) * 1e3
+    _, ids, taus, _, _, _ = eng._pending
+    ids[:] = 0          # the caller reuses its buffers right away
+    taus[:] = 1.0
+    recs = eng.sweep_fetch()
+    for f in ref.dtype.names:
+        if f == "exec_passes":  # memo hits depend on which CTA ran what
+            continue
+        assert np.ascontiguousarray(recs[f]).tobytes() == np.ascontiguousarray(ref[f]).tobytes(), f
+    assert kernel_ms > 50.0, kernel_ms  # a launch long enough for the timing to mean something
+    assert call_ms < 0.5 * kernel_ms, (call_ms, kernel_ms)
