@@ -1,2 +1,5 @@
 #include "rw_inst.cuh"
-RW_INSTANTIATE(8, 16, 256)
+#ifndef RW_L8
+#define RW_L8 16  // rows per warp block / 32 (experiment: -DRW_L8=8)
+#endif
+RW_INSTANTIATE(8, RW_L8, 256)
